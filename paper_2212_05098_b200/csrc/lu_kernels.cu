@@ -1,0 +1,521 @@
+// lu_kernels.cu -- sm_100a kernels K1..K4 and the C-ABI entry points of
+// liblaneutf_b200.so (declared in include/laneutf_b200.h).
+//
+// One launch per call: K1/K2 are single-pass (classify/validate -> decoupled
+// look-back scan -> scatter) over 16 KiB tiles; K3/K4 are read-only
+// validators that reduce the first bad position with one atomic per
+// erroneous tile and finalize in the last CTA.  Stream-ordered; the library
+// allocates nothing and keeps no mutable global state (per-call workspace,
+// thread-local error string).
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "lu_common.cuh"
+#include "lu_utf16.cuh"
+#include "lu_utf8.cuh"
+
+#include "../../include/laneutf_b200.h"
+
+namespace lu {
+
+constexpr int kOutStrideU16 = kChunkBytes + 16;      // words per warp staging region (<= 1 word per byte)
+constexpr int kOutStrideU8 = 3 * kChunkBytes / 2 + 32; // bytes per warp region (<= 3 bytes per word)
+
+constexpr size_t kInSmemBytes = sizeof(uint32_t) * kInWords;
+constexpr size_t kSmemK1 = kInSmemBytes + sizeof(uint16_t) * kOutStrideU16 * kWarps;
+constexpr size_t kSmemK2 = kInSmemBytes + kOutStrideU8 * kWarps;
+constexpr size_t kSmemVal = kInSmemBytes;
+
+struct TileShared {
+    WarpResult wres[kWarps];
+    uint32_t warp_excl[kWarps];
+    uint64_t excl;
+    uint32_t first_err_warp;
+    uint32_t tile_units;
+    uint32_t skip;
+};
+
+// ------------------------------------------------------------- copy-out
+
+// Copy cnt UTF-16 words from shared memory (16-byte aligned region) to the
+// output at word index g0 of the 16-byte aligned frame out_a (so 16-byte
+// chunks are aligned); partial head/tail chunks go word by word.
+__device__ __forceinline__ void copy_out_u16(const uint16_t *src, uint32_t cnt, uint16_t *out_a, uint64_t g0)
+{
+    if (cnt == 0)
+        return;
+    const uint32_t lane = lane_id();
+    const uint64_t g_end = g0 + cnt;
+    const uint64_t a0 = g0 & ~7ull;
+    const uint32_t shift = (uint32_t)(g0 - a0);
+    const uint32_t nchunks = (uint32_t)((g_end - a0 + 7) >> 3);
+    const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
+    for (uint32_t c = lane; c < nchunks; c += 32) {
+        const uint64_t a = a0 + 8ull * c;
+        const int32_t j = (int32_t)(8 * c) - (int32_t)shift;
+        if (a >= g0 && a + 8 <= g_end) {
+            uint4 v;
+            if ((shift & 1) == 0) {
+                const int m = j >> 1;
+                v = make_uint4(s32[m], s32[m + 1], s32[m + 2], s32[m + 3]);
+            } else {
+                const int m = (j - 1) >> 1;
+                const uint32_t w0 = s32[m], w1 = s32[m + 1], w2 = s32[m + 2], w3 = s32[m + 3], w4 = s32[m + 4];
+                v = make_uint4(prmt(w0, w1, 0x5432), prmt(w1, w2, 0x5432), prmt(w2, w3, 0x5432),
+                               prmt(w3, w4, 0x5432));
+            }
+            __stcs(reinterpret_cast<uint4 *>(out_a + a), v);
+        } else {
+            for (int k = 0; k < 8; ++k) {
+                const uint64_t g = a + k;
+                if (g >= g0 && g < g_end)
+                    out_a[g] = src[j + k];
+            }
+        }
+    }
+}
+
+// Same for bytes (UTF-8 output), 16-byte chunks.
+__device__ __forceinline__ void copy_out_u8(const uint8_t *src, uint32_t cnt, uint8_t *out_a, uint64_t g0)
+{
+    if (cnt == 0)
+        return;
+    const uint32_t lane = lane_id();
+    const uint64_t g_end = g0 + cnt;
+    const uint64_t a0 = g0 & ~15ull;
+    const uint32_t shift = (uint32_t)(g0 - a0);
+    const uint32_t nchunks = (uint32_t)((g_end - a0 + 15) >> 4);
+    const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
+    const uint32_t sh = 8u * ((16u - shift) & 3u); // byte shift inside the smem word
+    for (uint32_t c = lane; c < nchunks; c += 32) {
+        const uint64_t a = a0 + 16ull * c;
+        const int32_t j = (int32_t)(16 * c) - (int32_t)shift;
+        if (a >= g0 && a + 16 <= g_end) {
+            const int m = j >> 2; // floor (j >= 0 here)
+            uint4 v;
+            if (sh == 0) {
+                v = make_uint4(s32[m], s32[m + 1], s32[m + 2], s32[m + 3]);
+            } else {
+                const uint32_t w0 = s32[m], w1 = s32[m + 1], w2 = s32[m + 2], w3 = s32[m + 3], w4 = s32[m + 4];
+                v = make_uint4(fsr(w0, w1, sh), fsr(w1, w2, sh), fsr(w2, w3, sh), fsr(w3, w4, sh));
+            }
+            __stcs(reinterpret_cast<uint4 *>(out_a + a), v);
+        } else {
+            for (int k = 0; k < 16; ++k) {
+                const uint64_t g = a + k;
+                if (g >= g0 && g < g_end)
+                    out_a[g] = src[j + k];
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------- tile epilogue
+
+// Combine warp results (thread 0), look back (warp 0), broadcast.
+__device__ __forceinline__ void tile_scan(TileShared &ts, uint64_t *status)
+{
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0, first = kWarps;
+        for (int w = 0; w < kWarps; ++w) {
+            ts.warp_excl[w] = acc;
+            acc += ts.wres[w].units;
+            if (ts.wres[w].err) {
+                first = (uint32_t)w;
+                break;
+            }
+        }
+        ts.first_err_warp = first;
+        ts.tile_units = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const uint64_t agg = (ts.first_err_warp < kWarps ? kErrBit : 0ull) | (uint64_t)ts.tile_units;
+        const uint64_t ex = lookback(status, blockIdx.x, agg);
+        if (threadIdx.x == 0)
+            ts.excl = ex;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void sel_table_init(SelPair *sel)
+{
+    if (threadIdx.x < 16) {
+        const uint32_t idx = threadIdx.x;
+        uint32_t s[2] = {0, 0};
+        uint32_t j = 0;
+        for (uint32_t p = 0; p < 4; ++p) {
+            if (idx & (1u << p)) {
+                const uint32_t nib = p | ((4 + p) << 4);
+                s[j >> 1] |= nib << (8 * (j & 1));
+                ++j;
+            }
+        }
+        sel[idx].s01 = s[0];
+        sel[idx].s23 = s[1];
+    }
+}
+
+// ===================================================================== K1
+
+__global__ void __launch_bounds__(kThreads) k_utf8_to_utf16le(const uint8_t *__restrict__ base, uint32_t lead,
+                                                               uint64_t n, uint16_t *__restrict__ out_a,
+                                                               uint32_t out_lead_words, uint64_t *__restrict__ status,
+                                                               Outcome *__restrict__ res, uint32_t ntiles)
+{
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint32_t *in_s = reinterpret_cast<uint32_t *>(smem_raw);
+    uint16_t *out_s = reinterpret_cast<uint16_t *>(smem_raw + kInSmemBytes);
+    __shared__ SelPair sel[16];
+    __shared__ TileShared ts;
+
+    const int64_t tile_off = (int64_t)blockIdx.x * kTileBytes;
+    const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n;
+    const bool interior = stage_tile(in_s, base, tile_off, lo_b, hi_b);
+    sel_table_init(sel);
+    __syncthreads();
+
+    const uint32_t warp = threadIdx.x >> 5;
+    uint16_t *out_w = out_s + warp * kOutStrideU16;
+    if (interior)
+        u8u16_warp<false>(in_s, out_w, sel, tile_off, lo_b, hi_b, ts.wres[warp]);
+    else
+        u8u16_warp<true>(in_s, out_w, sel, tile_off, lo_b, hi_b, ts.wres[warp]);
+    __syncthreads();
+    tile_scan(ts, status);
+
+    const uint64_t ex = ts.excl;
+    if (ex & kErrBit)
+        return; // an earlier tile holds the first error: nothing here is output
+    const uint32_t first = ts.first_err_warp;
+    if (warp <= first && warp < kWarps) {
+        const uint64_t g0 = (ex & kValMask) + ts.warp_excl[warp] + out_lead_words;
+        copy_out_u16(out_w, ts.wres[warp].units, out_a, g0);
+    }
+    if (threadIdx.x == 0) {
+        const uint64_t written = (ex & kValMask) + ts.tile_units;
+        if (first < kWarps) {
+            res->status = kStatusMalformed;
+            res->pad = 0;
+            res->consumed = (uint64_t)(tile_off + ts.wres[first].pos - lo_b);
+            res->written = written;
+        } else if (blockIdx.x == ntiles - 1) {
+            res->status = kStatusOk;
+            res->pad = 0;
+            res->consumed = n;
+            res->written = written;
+        }
+    }
+}
+
+// ===================================================================== K2
+
+__global__ void __launch_bounds__(kThreads) k_utf16le_to_utf8(const uint8_t *__restrict__ base, uint32_t lead,
+                                                               uint64_t n_words, uint8_t *__restrict__ out_a,
+                                                               uint32_t out_lead, uint64_t *__restrict__ status,
+                                                               Outcome *__restrict__ res, uint32_t ntiles)
+{
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint32_t *in_s = reinterpret_cast<uint32_t *>(smem_raw);
+    uint8_t *out_s = smem_raw + kInSmemBytes;
+    __shared__ TileShared ts;
+
+    const int64_t tile_off = (int64_t)blockIdx.x * kTileBytes;
+    const int64_t lo_b = lead, hi_b = (int64_t)lead + 2 * (int64_t)n_words;
+    const bool interior = stage_tile(in_s, base, tile_off, lo_b, hi_b);
+    __syncthreads();
+
+    const uint32_t warp = threadIdx.x >> 5;
+    uint8_t *out_w = out_s + warp * kOutStrideU8;
+    if (interior)
+        u16u8_warp<false>(in_s, out_w, tile_off, lo_b, hi_b, ts.wres[warp]);
+    else
+        u16u8_warp<true>(in_s, out_w, tile_off, lo_b, hi_b, ts.wres[warp]);
+    __syncthreads();
+    tile_scan(ts, status);
+
+    const uint64_t ex = ts.excl;
+    if (ex & kErrBit)
+        return;
+    const uint32_t first = ts.first_err_warp;
+    if (warp <= first && warp < kWarps) {
+        const uint64_t g0 = (ex & kValMask) + ts.warp_excl[warp] + out_lead;
+        copy_out_u8(out_w, ts.wres[warp].units, out_a, g0);
+    }
+    if (threadIdx.x == 0) {
+        const uint64_t written = (ex & kValMask) + ts.tile_units;
+        if (first < kWarps) {
+            res->status = kStatusMalformed;
+            res->pad = 0;
+            res->consumed = (uint64_t)((tile_off + ts.wres[first].pos - lo_b) >> 1);
+            res->written = written;
+        } else if (blockIdx.x == ntiles - 1) {
+            res->status = kStatusOk;
+            res->pad = 0;
+            res->consumed = n_words;
+            res->written = written;
+        }
+    }
+}
+
+// ================================================================= K3 / K4
+
+// ws layout for the validators: [u64 max(n - bad_pos)][u32 done][u32 pad]
+template <bool Utf16>
+__global__ void __launch_bounds__(kThreads) k_validate(const uint8_t *__restrict__ base, uint32_t lead, uint64_t n,
+                                                       uint64_t *__restrict__ ws, Outcome *__restrict__ res,
+                                                       uint32_t ntiles)
+{
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint32_t *in_s = reinterpret_cast<uint32_t *>(smem_raw);
+    __shared__ TileShared ts;
+    const uint64_t n_bytes = Utf16 ? 2 * n : n;
+    const int64_t tile_off = (int64_t)blockIdx.x * kTileBytes;
+    const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n_bytes;
+
+    if (threadIdx.x == 0) {
+        // a tile that starts after an already-found error has nothing to
+        // decide (the reference stops at the first error too)
+        const uint64_t best = *reinterpret_cast<volatile uint64_t *>(ws);
+        const int64_t bad_b = lo_b + (Utf16 ? 2 : 1) * (int64_t)(n - best);
+        ts.skip = best != 0 && bad_b < tile_off;
+    }
+    __syncthreads();
+    if (!ts.skip) {
+        const bool interior = stage_tile(in_s, base, tile_off, lo_b, hi_b);
+        __syncthreads();
+        const uint32_t warp = threadIdx.x >> 5;
+        if (Utf16) {
+            if (interior)
+                u16val_warp<false>(in_s, tile_off, lo_b, hi_b, ts.wres[warp]);
+            else
+                u16val_warp<true>(in_s, tile_off, lo_b, hi_b, ts.wres[warp]);
+        } else {
+            if (interior)
+                u8val_warp<false>(in_s, tile_off, lo_b, hi_b, ts.wres[warp]);
+            else
+                u8val_warp<true>(in_s, tile_off, lo_b, hi_b, ts.wres[warp]);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 0; w < kWarps; ++w) {
+                if (ts.wres[w].err) {
+                    const int64_t pb = tile_off + ts.wres[w].pos - lo_b; // byte position
+                    const uint64_t pu = Utf16 ? (uint64_t)(pb >> 1) : (uint64_t)pb;
+                    atomicMax(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)(n - pu));
+                    break;
+                }
+            }
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t prev = atomicAdd(reinterpret_cast<unsigned int *>(ws + 1), 1u);
+        if (prev == ntiles - 1) {
+            __threadfence();
+            const uint64_t best = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 0ull);
+            res->status = best ? kStatusMalformed : kStatusOk;
+            res->pad = 0;
+            res->consumed = n - best;
+            res->written = 0;
+        }
+    }
+}
+
+// =============================================================== host side
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char *msg)
+{
+    g_err = msg;
+    return code;
+}
+
+static int cuda_fail(cudaError_t e, const char *what)
+{
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return LU_ERR_CUDA;
+}
+
+static uint64_t n_tiles(uint64_t bytes, uint32_t lead)
+{
+    uint64_t t = (bytes + lead + kTileBytes - 1) / kTileBytes;
+    return t ? t : 1;
+}
+
+static int set_smem_attrs()
+{
+    static std::once_flag once;
+    static cudaError_t status = cudaSuccess;
+    std::call_once(once, [] {
+        cudaError_t e;
+        e = cudaFuncSetAttribute(k_utf8_to_utf16le, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemK1);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_utf16le_to_utf8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemK2);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_validate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSmemVal);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_validate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemVal);
+        status = e;
+    });
+    if (status != cudaSuccess)
+        return cuda_fail(status, "cudaFuncSetAttribute");
+    return 0;
+}
+
+} // namespace lu
+
+using namespace lu;
+
+extern "C" {
+
+const char *lu_last_error(void) { return g_err.c_str(); }
+
+const char *lu_version(void) { return "laneutf_b200 0.1.0 (sm_100a)"; }
+
+uint64_t lu_workspace_bytes(int op, uint64_t n_units)
+{
+    switch (op) {
+    case LU_OP_UTF8_TO_UTF16LE:
+        return 8 * (n_tiles(n_units, 15) + 1) + 64;
+    case LU_OP_UTF16LE_TO_UTF8:
+        return 8 * (n_tiles(2 * n_units, 15) + 1) + 64;
+    case LU_OP_VALIDATE_UTF8:
+    case LU_OP_VALIDATE_UTF16LE:
+        return 64;
+    default:
+        return 0;
+    }
+}
+
+int lu_device_supported(int dev)
+{
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) != cudaSuccess)
+        return 0;
+    return p.major == 10 && p.minor == 0;
+}
+
+int lu_tile_bytes(void) { return kTileBytes; }
+
+int lu_utf8_to_utf16le(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint64_t out_cap_words, void *ws,
+                       uint64_t ws_bytes, lu_outcome *res, cudaStream_t stream)
+{
+    if ((!in && n_bytes) || !res || !ws)
+        return fail(LU_ERR_INVALID, "null pointer");
+    if (((uintptr_t)out & 1) || ((uintptr_t)ws & 7) || ((uintptr_t)res & 7))
+        return fail(LU_ERR_INVALID, "misaligned out/ws/res pointer");
+    if (out_cap_words < n_bytes)
+        return fail(LU_ERR_CAPACITY, "output capacity below the worst case (1 word per input byte)");
+    if (!out && n_bytes)
+        return fail(LU_ERR_INVALID, "null output");
+    const uint32_t lead = (uint32_t)((uintptr_t)in & 15);
+    const uint64_t nt = n_tiles(n_bytes, lead);
+    if (ws_bytes < 8 * nt)
+        return fail(LU_ERR_WORKSPACE, "workspace too small (see lu_workspace_bytes)");
+    if (nt > 0x7fffffffull)
+        return fail(LU_ERR_INVALID, "input too large");
+    int rc = set_smem_attrs();
+    if (rc)
+        return rc;
+    cudaError_t e = cudaMemsetAsync(ws, 0, 8 * nt, stream);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "cudaMemsetAsync");
+    const uint8_t *base = in ? in - lead : reinterpret_cast<const uint8_t *>(16);
+    uint16_t *out_safe = out ? out : reinterpret_cast<uint16_t *>(16);
+    const uint32_t out_lead = (uint32_t)(((uintptr_t)out_safe & 15) >> 1);
+    uint16_t *out_a = out_safe - out_lead;
+    k_utf8_to_utf16le<<<(unsigned)nt, kThreads, kSmemK1, stream>>>(base, lead, n_bytes, out_a, out_lead,
+                                                                   reinterpret_cast<uint64_t *>(ws),
+                                                                   reinterpret_cast<Outcome *>(res), (uint32_t)nt);
+    e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return cuda_fail(e, "k_utf8_to_utf16le launch");
+    return 0;
+}
+
+int lu_utf16le_to_utf8(const uint16_t *in, uint64_t n_words, uint8_t *out, uint64_t out_cap_bytes, void *ws,
+                       uint64_t ws_bytes, lu_outcome *res, cudaStream_t stream)
+{
+    if ((!in && n_words) || !res || !ws)
+        return fail(LU_ERR_INVALID, "null pointer");
+    if (((uintptr_t)in & 1) || ((uintptr_t)ws & 7) || ((uintptr_t)res & 7))
+        return fail(LU_ERR_INVALID, "misaligned in/ws/res pointer");
+    if (out_cap_bytes < 3 * n_words)
+        return fail(LU_ERR_CAPACITY, "output capacity below the worst case (3 bytes per input word)");
+    if (!out && n_words)
+        return fail(LU_ERR_INVALID, "null output");
+    const uint8_t *inb = reinterpret_cast<const uint8_t *>(in);
+    const uint32_t lead = (uint32_t)((uintptr_t)inb & 15);
+    const uint64_t nt = n_tiles(2 * n_words, lead);
+    if (ws_bytes < 8 * nt)
+        return fail(LU_ERR_WORKSPACE, "workspace too small (see lu_workspace_bytes)");
+    if (nt > 0x7fffffffull)
+        return fail(LU_ERR_INVALID, "input too large");
+    int rc = set_smem_attrs();
+    if (rc)
+        return rc;
+    cudaError_t e = cudaMemsetAsync(ws, 0, 8 * nt, stream);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "cudaMemsetAsync");
+    const uint8_t *base = inb ? inb - lead : reinterpret_cast<const uint8_t *>(16);
+    uint8_t *out_safe = out ? out : reinterpret_cast<uint8_t *>(16);
+    const uint32_t out_lead = (uint32_t)((uintptr_t)out_safe & 15);
+    k_utf16le_to_utf8<<<(unsigned)nt, kThreads, kSmemK2, stream>>>(base, lead, n_words, out_safe - out_lead,
+                                                                   out_lead, reinterpret_cast<uint64_t *>(ws),
+                                                                   reinterpret_cast<Outcome *>(res), (uint32_t)nt);
+    e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return cuda_fail(e, "k_utf16le_to_utf8 launch");
+    return 0;
+}
+
+static int validate_impl(bool utf16, const uint8_t *inb, uint64_t n_units, void *ws, uint64_t ws_bytes,
+                         lu_outcome *res, cudaStream_t stream)
+{
+    if ((!inb && n_units) || !res || !ws)
+        return fail(LU_ERR_INVALID, "null pointer");
+    if ((utf16 && ((uintptr_t)inb & 1)) || ((uintptr_t)ws & 7) || ((uintptr_t)res & 7))
+        return fail(LU_ERR_INVALID, "misaligned in/ws/res pointer");
+    if (ws_bytes < 16)
+        return fail(LU_ERR_WORKSPACE, "workspace too small (see lu_workspace_bytes)");
+    const uint32_t lead = (uint32_t)((uintptr_t)inb & 15);
+    const uint64_t nt = n_tiles(utf16 ? 2 * n_units : n_units, lead);
+    if (nt > 0x7fffffffull)
+        return fail(LU_ERR_INVALID, "input too large");
+    int rc = set_smem_attrs();
+    if (rc)
+        return rc;
+    cudaError_t e = cudaMemsetAsync(ws, 0, 16, stream);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "cudaMemsetAsync");
+    const uint8_t *base = inb ? inb - lead : reinterpret_cast<const uint8_t *>(16);
+    if (utf16)
+        k_validate<true><<<(unsigned)nt, kThreads, kSmemVal, stream>>>(
+            base, lead, n_units, reinterpret_cast<uint64_t *>(ws), reinterpret_cast<Outcome *>(res), (uint32_t)nt);
+    else
+        k_validate<false><<<(unsigned)nt, kThreads, kSmemVal, stream>>>(
+            base, lead, n_units, reinterpret_cast<uint64_t *>(ws), reinterpret_cast<Outcome *>(res), (uint32_t)nt);
+    e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return cuda_fail(e, "k_validate launch");
+    return 0;
+}
+
+int lu_validate_utf8(const uint8_t *in, uint64_t n_bytes, void *ws, uint64_t ws_bytes, lu_outcome *res,
+                     cudaStream_t stream)
+{
+    return validate_impl(false, in, n_bytes, ws, ws_bytes, res, stream);
+}
+
+int lu_validate_utf16le(const uint16_t *in, uint64_t n_words, void *ws, uint64_t ws_bytes, lu_outcome *res,
+                        cudaStream_t stream)
+{
+    return validate_impl(true, reinterpret_cast<const uint8_t *>(in), n_words, ws, ws_bytes, res, stream);
+}
+
+} // extern "C"

@@ -1,0 +1,208 @@
+// lu_utf16.cuh -- UTF-16LE side: K2 utf16le -> utf8 transcode, K4 validate.
+//
+// Semantics = laneutf.scalar.transcode_utf16le_to_utf8 / validate_utf16le
+// (/root/reference/pkg/src/laneutf/scalar.py:108-147, 200-217).  Word i is bad
+// iff it is a high surrogate not followed by a low one, or a low surrogate not
+// preceded by a high one -- an exact local predicate, so
+// the detector IS the exact check here.  Output bytes per word: 1 (< 0x80),
+// 2 (< 0x800), 3 (other non-surrogates), 4 for a high surrogate that starts a
+// pair, 0 for the low surrogate that ends one.  A lane holds one 32-bit quad
+// = two words; a 128-byte warp step covers 64 words.
+#pragma once
+
+#include "lu_common.cuh"
+#include "lu_utf8.cuh" // WarpResult
+
+namespace lu {
+
+__device__ __forceinline__ bool is_hs(uint32_t w) { return (w & 0xFC00u) == 0xD800u; }
+__device__ __forceinline__ bool is_ls(uint32_t w) { return (w & 0xFC00u) == 0xDC00u; }
+
+// UTF-8 bytes of one word (pair-aware), little-endian packed, and their count.
+// Bad words get a bounded garbage encoding (<= 3 bytes): nothing at or after
+// the first bad word is ever copied out.
+__device__ __forceinline__ void u16_encode(uint32_t w, uint32_t wprev, uint32_t wnext, uint32_t &u, uint32_t &len)
+{
+    const bool hs = is_hs(w), ls = is_ls(w);
+    if (hs && is_ls(wnext)) {
+        const uint32_t cp = 0x10000u + (((w - 0xD800u) << 10) | (wnext - 0xDC00u));
+        u = (0xF0u | (cp >> 18)) | ((0x80u | ((cp >> 12) & 0x3Fu)) << 8) | ((0x80u | ((cp >> 6) & 0x3Fu)) << 16) |
+            ((0x80u | (cp & 0x3Fu)) << 24);
+        len = 4;
+    } else if (ls && is_hs(wprev)) {
+        u = 0;
+        len = 0;
+    } else if (w < 0x80u) {
+        u = w;
+        len = 1;
+    } else if (w < 0x800u) {
+        u = (0xC0u | (w >> 6)) | ((0x80u | (w & 0x3Fu)) << 8);
+        len = 2;
+    } else {
+        u = (0xE0u | (w >> 12)) | ((0x80u | ((w >> 6) & 0x3Fu)) << 8) | ((0x80u | (w & 0x3Fu)) << 16);
+        len = 3;
+    }
+}
+
+// bad bits for the two words of a quad: bit 0 = low word, bit 1 = high word
+__device__ __forceinline__ uint32_t u16_bad2(uint32_t w0, uint32_t w1, uint32_t wp, uint32_t wn)
+{
+    const uint32_t b0 = (is_hs(w0) && !is_ls(w1)) || (is_ls(w0) && !is_hs(wp));
+    const uint32_t b1 = (is_hs(w1) && !is_ls(wn)) || (is_ls(w1) && !is_hs(w0));
+    return b0 | (b1 << 1);
+}
+
+// fast any-surrogate test for a quad
+__device__ __forceinline__ bool u16_any_sur(uint32_t x)
+{
+    const uint32_t t = (x & 0xF800F800u) ^ 0xD800D800u; // zero half iff surrogate
+    return ((t & 0xFFFFu) == 0) || ((t >> 16) == 0);
+}
+
+// valid-word bits (bit 0 low word, bit 1 high word) for boundary tiles
+__device__ __forceinline__ uint32_t valid_words(int64_t a, int64_t lo, int64_t hi)
+{
+    return (uint32_t)(a >= lo && a + 2 <= hi) | ((uint32_t)(a + 2 >= lo && a + 4 <= hi) << 1);
+}
+
+template <bool Boundary>
+__device__ __forceinline__ void u16u8_warp(const uint32_t *in_s, uint8_t *out_w, int64_t tile_off, int64_t lo_b,
+                                           int64_t hi_b, WarpResult &wr)
+{
+    const uint32_t lane = lane_id();
+    const uint32_t warp = threadIdx.x >> 5;
+    const int q0 = kInHead + (int)warp * kChunkQuads;
+    uint32_t running = 0;
+    uint32_t err = 0, err_pos = 0, units = 0;
+
+#pragma unroll 1
+    for (int g = 0; g < kGroups; ++g) {
+        uint32_t u0[kGroup], u1[kGroup], l0[kGroup], l1[kGroup], bad[kGroup];
+        uint32_t pk = 0, anybad = 0;
+        const int qg = q0 + g * kGroup * 32;
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) {
+            const int q = qg + j * 32 + (int)lane;
+            const uint32_t x = in_s[q];
+            const uint32_t xp = in_s[q - 1];
+            const uint32_t xn = in_s[q + 1];
+            const uint32_t w0 = x & 0xFFFFu, w1 = x >> 16, wp = xp >> 16, wn = xn & 0xFFFFu;
+            u16_encode(w0, wp, w1, u0[j], l0[j]);
+            u16_encode(w1, w0, wn, u1[j], l1[j]);
+            bad[j] = 0;
+            if (__any_sync(0xffffffffu, u16_any_sur(x) || is_ls(wn)))
+                bad[j] = u16_bad2(w0, w1, wp, wn);
+            if (Boundary) {
+                const int64_t a = tile_off + 4 * (int64_t)(q - kInHead);
+                const uint32_t v = valid_words(a, lo_b, hi_b);
+                if (!(v & 1))
+                    l0[j] = 0;
+                if (!(v & 2))
+                    l1[j] = 0;
+                bad[j] &= v;
+            }
+            anybad |= bad[j];
+            pk |= (l0[j] + l1[j]) << (8 * j);
+        }
+        const uint32_t incl = warp_scan_packed(pk);
+        const uint32_t excl = incl - pk;
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+
+        if (__any_sync(0xffffffffu, anybad != 0)) {
+            uint32_t before = running;
+            bool found = false;
+#pragma unroll
+            for (int j = 0; j < kGroup; ++j) {
+                if (!found) {
+                    const uint32_t bm = __ballot_sync(0xffffffffu, bad[j] != 0);
+                    if (bm) {
+                        const uint32_t fl = (uint32_t)__ffs(bm) - 1;
+                        const uint32_t which = (bad[j] & 1) ? 0u : 1u;
+                        const uint32_t within = ((excl >> (8 * j)) & 0xFFu) + (which ? l0[j] : 0u);
+                        const uint32_t wf = __shfl_sync(0xffffffffu, within, fl);
+                        const uint32_t whf = __shfl_sync(0xffffffffu, which, fl);
+                        err = 1;
+                        // tile-relative byte offset of the bad word
+                        err_pos = 4u * (uint32_t)(qg + j * 32 + (int)fl - kInHead) + 2u * whf;
+                        units = before + wf;
+                        found = true;
+                    }
+                }
+                before += (tot >> (8 * j)) & 0xFFu;
+            }
+        }
+
+        uint32_t base = running;
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) {
+            const uint32_t off = base + ((excl >> (8 * j)) & 0xFFu);
+            const uint64_t p = (uint64_t)u0[j] | ((uint64_t)u1[j] << (8 * l0[j]));
+            const uint32_t pl = (uint32_t)p, ph = (uint32_t)(p >> 32);
+            const uint32_t n = l0[j] + l1[j];
+            uint8_t *dst = out_w + off;
+            if (n > 0)
+                dst[0] = (uint8_t)pl;
+            if (n > 1)
+                dst[1] = (uint8_t)(pl >> 8);
+            if (n > 2)
+                dst[2] = (uint8_t)(pl >> 16);
+            if (n > 3)
+                dst[3] = (uint8_t)(pl >> 24);
+            if (n > 4)
+                dst[4] = (uint8_t)ph;
+            if (n > 5)
+                dst[5] = (uint8_t)(ph >> 8);
+            if (n > 6)
+                dst[6] = (uint8_t)(ph >> 16);
+            base += (tot >> (8 * j)) & 0xFFu;
+        }
+        running = base;
+        if (err)
+            break;
+    }
+    if (!err)
+        units = running;
+    if (lane == 0) {
+        wr.err = err;
+        wr.pos = err_pos;
+        wr.units = units;
+    }
+}
+
+template <bool Boundary>
+__device__ __forceinline__ void u16val_warp(const uint32_t *in_s, int64_t tile_off, int64_t lo_b, int64_t hi_b,
+                                            WarpResult &wr)
+{
+    const uint32_t lane = lane_id();
+    const uint32_t warp = threadIdx.x >> 5;
+    const int q0 = kInHead + (int)warp * kChunkQuads;
+    uint32_t err = 0, err_pos = 0;
+#pragma unroll 4
+    for (int s = 0; s < kSteps; ++s) {
+        const int q = q0 + s * 32 + (int)lane;
+        const uint32_t x = in_s[q];
+        const uint32_t xn = in_s[q + 1];
+        uint32_t bad = 0;
+        if (__any_sync(0xffffffffu, u16_any_sur(x) || is_ls(xn & 0xFFFFu))) {
+            const uint32_t xp = in_s[q - 1];
+            bad = u16_bad2(x & 0xFFFFu, x >> 16, xp >> 16, xn & 0xFFFFu);
+            if (Boundary)
+                bad &= valid_words(tile_off + 4 * (int64_t)(q - kInHead), lo_b, hi_b);
+        }
+        const uint32_t bm = __ballot_sync(0xffffffffu, bad != 0);
+        if (bm) {
+            const uint32_t fl = (uint32_t)__ffs(bm) - 1;
+            const uint32_t which = __shfl_sync(0xffffffffu, (bad & 1) ? 0u : 1u, fl);
+            err = 1;
+            err_pos = 4u * (uint32_t)(q0 + s * 32 + (int)fl - kInHead) + 2u * which;
+            break;
+        }
+    }
+    if (lane == 0) {
+        wr.err = err;
+        wr.pos = err_pos;
+        wr.units = 0;
+    }
+}
+
+} // namespace lu

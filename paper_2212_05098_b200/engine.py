@@ -1,0 +1,385 @@
+"""Entry points with the reference facade's signatures, backed by the B200 engine.
+
+Mirrors ``laneutf.engine`` (/root/reference/pkg/src/laneutf/engine.py):
+``transcode`` (178-209), ``transcode_to_bytes`` (212-223), ``validate``
+(226-240), ``EngineKind``/``parse_engine`` (58-103), ``detect`` (141-153),
+``resolve_engine`` with the ``LANEUTF_ENGINE`` override (156-163),
+``worst_case_output_bytes`` (171-175) and ``swap_utf16_byte_order``
+(243-250).  Same argument meaning, return values and error behaviour:
+malformed input is a status, never an exception; ``ValueError`` for an
+unknown direction, an unparsable or unavailable engine, and odd UTF-16 byte
+lengths (raised before any device work).
+
+This build fills the reference's reserved ``native`` slot (engine.py:1-16,
+194-200) with the sm_100a engine and is the default engine.  The reference's
+CPU engines (``scalar``, ``emulated(n)``) are parsed for compatibility but
+are not part of this build: asking for one raises ``ValueError`` exactly like
+the reference does for an engine missing from its inventory.  There is no CPU
+fallback anywhere on this path.
+
+Beyond the reference signatures, ``data`` / ``out`` may also be torch tensors:
+a CUDA tensor stays on the device (zero-copy), a pinned CPU tensor is copied
+asynchronously.  ``transcode_device`` is the stream-ordered, device-resident
+form used by the benchmark and the multi-GPU driver.
+"""
+
+from __future__ import annotations
+
+import os
+import warnings
+from dataclasses import dataclass
+from functools import lru_cache
+
+import numpy as np
+import torch
+
+from . import _native
+from .outcome import STATUS_BY_CODE, TranscodeOutcome, TranscodeStatus
+
+__all__ = [
+    "UTF8_TO_UTF16",
+    "UTF16_TO_UTF8",
+    "DIRECTIONS",
+    "ENGINE_ENV_VAR",
+    "EngineKind",
+    "EngineInventory",
+    "parse_engine",
+    "resolve_engine",
+    "detect",
+    "transcode",
+    "transcode_to_bytes",
+    "validate",
+    "transcode_device",
+    "validate_device",
+    "outcome_from_tensor",
+    "swap_utf16_byte_order",
+    "worst_case_output_bytes",
+]
+
+UTF8_TO_UTF16 = "utf8-to-utf16"
+UTF16_TO_UTF8 = "utf16-to-utf8"
+DIRECTIONS = (UTF8_TO_UTF16, UTF16_TO_UTF8)
+
+ENGINE_ENV_VAR = "LANEUTF_ENGINE"
+
+
+@dataclass(frozen=True)
+class EngineKind:
+    """A selectable backend: ``scalar``, ``emulated(n)``, or ``native`` (engine.py:58-86)."""
+
+    family: str
+    lane_count: int | None = None
+
+    def __post_init__(self):
+        if self.family not in ("scalar", "emulated", "native"):
+            raise ValueError(f"unknown engine family {self.family!r}")
+        if (self.family == "emulated") != (self.lane_count is not None):
+            raise ValueError("lane_count is for emulated engines only")
+
+    @classmethod
+    def scalar_kind(cls) -> "EngineKind":
+        return cls("scalar")
+
+    @classmethod
+    def emulated(cls, lane_count: int) -> "EngineKind":
+        return cls("emulated", lane_count)
+
+    @classmethod
+    def native(cls) -> "EngineKind":
+        return cls("native")
+
+    def describe(self) -> str:
+        if self.family == "emulated":
+            return f"emulated({self.lane_count})"
+        return self.family
+
+
+def parse_engine(text: str) -> EngineKind:
+    """Accepts ``scalar``, ``native``, ``emulated``, ``emulated-N``, ``emulated(N)`` (engine.py:89-103)."""
+    name = text.strip().lower()
+    if name == "scalar":
+        return EngineKind.scalar_kind()
+    if name == "native":
+        return EngineKind.native()
+    if name == "emulated":
+        return EngineKind.emulated(64)
+    for prefix, suffix in (("emulated-", ""), ("emulated(", ")")):
+        if name.startswith(prefix) and name.endswith(suffix) and len(name) > len(prefix) + len(suffix):
+            body = name[len(prefix) : len(name) - len(suffix)]
+            if body.isdigit():
+                return EngineKind.emulated(int(body))
+    raise ValueError(f"cannot parse engine name {text!r}")
+
+
+@dataclass(frozen=True)
+class EngineInventory:
+    kinds: tuple[EngineKind, ...]
+    device_name: str | None
+    native_capable_host: bool
+    reason: str | None = None
+
+    def available(self, kind: EngineKind) -> bool:
+        return kind in self.kinds
+
+
+@lru_cache(maxsize=1)
+def detect() -> EngineInventory:
+    """Enumerate usable engines; stable for the life of the process (engine.py:141-153)."""
+    reason = _native.unavailable_reason()
+    name = torch.cuda.get_device_name() if torch.cuda.is_available() else None
+    kinds = (EngineKind.native(),) if reason is None else ()
+    return EngineInventory(kinds=kinds, device_name=name, native_capable_host=reason is None, reason=reason)
+
+
+def resolve_engine(engine: EngineKind | str | None = None) -> EngineKind:
+    """Engine named by the argument, else the environment, else ``native``."""
+    if engine is None:
+        named = os.environ.get(ENGINE_ENV_VAR)
+        return parse_engine(named) if named else EngineKind.native()
+    if isinstance(engine, str):
+        return parse_engine(engine)
+    return engine
+
+
+def _check_direction(direction: str) -> None:
+    if direction not in DIRECTIONS:
+        raise ValueError(f"direction must be one of {DIRECTIONS}")
+
+
+def _require_native(kind: EngineKind) -> None:
+    if kind.family != "native":
+        raise ValueError(
+            f"{kind.describe()} engine unavailable: this build ships only the native B200 engine "
+            "(the CPU engines live in the reference laneutf package)"
+        )
+    inventory = detect()
+    if not inventory.available(kind):
+        raise ValueError(f"native engine unavailable: {inventory.reason}")
+
+
+def worst_case_output_bytes(direction: str, input_length: int) -> int:
+    """engine.py:171-175."""
+    _check_direction(direction)
+    if direction == UTF8_TO_UTF16:
+        return 2 * input_length
+    return 3 * (input_length // 2)
+
+
+# ------------------------------------------------------------------ buffers
+
+
+def _device() -> torch.device:
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _byte_len(data) -> int:
+    if isinstance(data, torch.Tensor):
+        return data.numel() * data.element_size()
+    if isinstance(data, np.ndarray):
+        return data.nbytes
+    return memoryview(data).nbytes
+
+
+def _to_device_bytes(data, device: torch.device) -> torch.Tensor:
+    """Input as a contiguous uint8 CUDA tensor (zero-copy when already there)."""
+    if isinstance(data, torch.Tensor):
+        t = data.contiguous()
+        if t.dtype != torch.uint8:
+            t = t.view(torch.uint8) if t.numel() else torch.empty(0, dtype=torch.uint8)
+        t = t.reshape(-1)
+        if t.is_cuda:
+            return t if t.device == device else t.to(device)
+        return t.to(device, non_blocking=t.is_pinned())
+    if isinstance(data, np.ndarray):
+        arr = np.ascontiguousarray(data).view(np.uint8).reshape(-1)
+    else:
+        arr = np.frombuffer(memoryview(data).cast("B"), dtype=np.uint8)
+    if arr.size == 0:
+        return torch.empty(0, dtype=torch.uint8, device=device)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")  # read-only host buffers are only read
+        host = torch.from_numpy(arr)
+    return host.to(device)
+
+
+def outcome_from_tensor(res: torch.Tensor) -> TranscodeOutcome:
+    """Decode a device/host lu_outcome (3 x int64: status|pad, consumed, written)."""
+    v = res.view(torch.int64)[:3].tolist()
+    status = STATUS_BY_CODE[int(v[0]) & 0xFFFFFFFF]
+    return TranscodeOutcome(status, int(v[1]), int(v[2]))
+
+
+def transcode_device(
+    direction: str,
+    src: torch.Tensor,
+    out: torch.Tensor | None = None,
+    *,
+    res: torch.Tensor | None = None,
+    ws: torch.Tensor | None = None,
+    stream: torch.cuda.Stream | None = None,
+) -> tuple[torch.Tensor, torch.Tensor]:
+    """Device-resident transcode, enqueued on ``stream``; no synchronisation.
+
+    ``src`` is a CUDA tensor holding the input bytes (UTF-8 bytes, or UTF-16LE
+    as uint8 of even length / int16 / uint16).  Returns ``(res, out)``:
+    ``res`` is an int64[3] CUDA tensor with the lu_outcome (decode with
+    ``outcome_from_tensor`` after the stream completes) and ``out`` the
+    worst-case output buffer (uint16 words or uint8 bytes).
+    """
+    _check_direction(direction)
+    device = src.device
+    srcb = _to_device_bytes(src, device)
+    nbytes = srcb.numel()
+    if direction == UTF8_TO_UTF16:
+        op, n_units, cap = _native.OP_UTF8_TO_UTF16LE, nbytes, nbytes
+        if out is None:
+            out = torch.empty(max(cap, 1), dtype=torch.uint16, device=device)
+        out_cap = out.numel() * out.element_size() // 2
+    else:
+        if nbytes % 2:
+            raise ValueError("UTF-16 input must be an even number of bytes")
+        op, n_units = _native.OP_UTF16LE_TO_UTF8, nbytes // 2
+        cap = 3 * n_units
+        if out is None:
+            out = torch.empty(max(cap, 1), dtype=torch.uint8, device=device)
+        out_cap = out.numel() * out.element_size()
+    if res is None:
+        res = torch.empty(3, dtype=torch.int64, device=device)
+    if ws is None:
+        ws = torch.empty(_native.workspace_bytes(op, n_units) // 8 + 1, dtype=torch.int64, device=device)
+    _native.launch(op, srcb, n_units, out, out_cap, ws, res, stream)
+    return res, out
+
+
+def validate_device(
+    direction: str,
+    src: torch.Tensor,
+    *,
+    res: torch.Tensor | None = None,
+    ws: torch.Tensor | None = None,
+    stream: torch.cuda.Stream | None = None,
+) -> torch.Tensor:
+    """Device-resident validation; returns the int64[3] outcome tensor."""
+    _check_direction(direction)
+    device = src.device
+    srcb = _to_device_bytes(src, device)
+    nbytes = srcb.numel()
+    if direction == UTF8_TO_UTF16:
+        op, n_units = _native.OP_VALIDATE_UTF8, nbytes
+    else:
+        if nbytes % 2:
+            raise ValueError("UTF-16 input must be an even number of bytes")
+        op, n_units = _native.OP_VALIDATE_UTF16LE, nbytes // 2
+    if res is None:
+        res = torch.empty(3, dtype=torch.int64, device=device)
+    if ws is None:
+        ws = torch.empty(_native.workspace_bytes(op, n_units) // 8 + 1, dtype=torch.int64, device=device)
+    _native.launch(op, srcb, n_units, None, 0, ws, res, stream)
+    return res
+
+
+# ------------------------------------------------------------- facade
+
+
+def _write_payload(out, payload: torch.Tensor) -> None:
+    """Copy the written prefix (a CUDA uint8 tensor) into the caller's ``out``."""
+    k = payload.numel()
+    if isinstance(out, torch.Tensor):
+        dst = out.view(torch.uint8).reshape(-1) if out.dtype != torch.uint8 else out.reshape(-1)
+        if dst.numel() < k:
+            raise ValueError("output buffer smaller than the transcoded payload")
+        dst[:k].copy_(payload, non_blocking=dst.is_cuda or dst.is_pinned())
+        if not dst.is_cuda:
+            torch.cuda.current_stream().synchronize()
+        return
+    mv = memoryview(out).cast("B")
+    if mv.readonly:
+        raise ValueError("output buffer is read-only")
+    if mv.nbytes < k:
+        raise ValueError("output buffer smaller than the transcoded payload")
+    if k:
+        host = torch.frombuffer(mv, dtype=torch.uint8, count=k)
+        host.copy_(payload)
+
+
+def transcode(
+    direction: str,
+    data,
+    out,
+    *,
+    engine: EngineKind | str | None = None,
+) -> TranscodeOutcome:
+    """Route one transcode call to the B200 engine (engine.py:178-209).
+
+    ``consumed`` and ``written`` count code units of the source and
+    destination formats.  ``out`` receives exactly the transcoded valid
+    prefix (``unit * written`` bytes); nothing past it is touched.
+    """
+    _check_direction(direction)
+    kind = resolve_engine(engine)
+    if direction == UTF16_TO_UTF8 and _byte_len(data) % 2:
+        raise ValueError("UTF-16 input must be an even number of bytes")
+    _require_native(kind)
+    device = _device()
+    src = _to_device_bytes(data, device)
+    out_dev = None
+    if isinstance(out, torch.Tensor) and out.is_cuda:
+        out_dev = out  # kernel writes straight into the caller's device buffer
+    res, buf = transcode_device(direction, src, out_dev)
+    outcome = outcome_from_tensor(res.cpu())
+    if out_dev is None:
+        unit = 2 if direction == UTF8_TO_UTF16 else 1
+        payload = buf.view(torch.uint8)[: unit * outcome.written]
+        _write_payload(out, payload)
+    return outcome
+
+
+def transcode_to_bytes(
+    direction: str,
+    data,
+    *,
+    engine: EngineKind | str | None = None,
+) -> tuple[TranscodeOutcome, bytes]:
+    """Transcode into a fresh worst-case buffer; returns outcome + payload (engine.py:212-223)."""
+    _check_direction(direction)
+    kind = resolve_engine(engine)
+    if direction == UTF16_TO_UTF8 and _byte_len(data) % 2:
+        raise ValueError("UTF-16 input must be an even number of bytes")
+    _require_native(kind)
+    device = _device()
+    src = _to_device_bytes(data, device)
+    res, buf = transcode_device(direction, src)
+    outcome = outcome_from_tensor(res.cpu())
+    unit = 2 if direction == UTF8_TO_UTF16 else 1
+    payload = buf.view(torch.uint8)[: unit * outcome.written].cpu().numpy().tobytes()
+    return outcome, payload
+
+
+def validate(
+    direction: str,
+    data,
+    *,
+    engine: EngineKind | str | None = None,
+) -> TranscodeOutcome:
+    """Validation via the B200 read-only kernels; written is always 0 (engine.py:226-240)."""
+    _check_direction(direction)
+    kind = resolve_engine(engine)
+    if direction == UTF16_TO_UTF8 and _byte_len(data) % 2:
+        raise ValueError("UTF-16 input must be an even number of bytes")
+    _require_native(kind)
+    device = _device()
+    src = _to_device_bytes(data, device)
+    res = validate_device(direction, src)
+    outcome = outcome_from_tensor(res.cpu())
+    return TranscodeOutcome(outcome.status, outcome.consumed, 0)
+
+
+def swap_utf16_byte_order(data: bytes) -> bytes:
+    """Byte-swap every 16-bit unit (LE <-> BE) (engine.py:243-250)."""
+    if len(data) % 2:
+        raise ValueError("UTF-16 input must have even byte length")
+    arr = np.frombuffer(memoryview(data).cast("B"), dtype=np.uint16)
+    return arr.byteswap().tobytes()
+
+
+__all__ += ["TranscodeOutcome", "TranscodeStatus"]

@@ -1,0 +1,315 @@
+"""Parity of the B200 engine (through the C ABI) with the oracle.
+
+Every comparison is bit-exact: status, consumed (= error offset), written and
+the payload bytes.  The oracle (oracle/) is pinned against the reference by
+tests/test_oracle.py.
+"""
+
+import random
+
+import numpy as np
+import pytest
+import torch
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+import oracle
+from paper_2212_05098_b200 import (
+    UTF8_TO_UTF16,
+    UTF16_TO_UTF8,
+    TranscodeStatus,
+    corpus,
+    outcome_from_tensor,
+    transcode,
+    transcode_device,
+    transcode_to_bytes,
+    validate,
+    validate_device,
+)
+
+from .helpers import payload_matches, words_to_bytes
+
+pytestmark = pytest.mark.gpu
+
+TILE = 16384
+
+
+def check_u8(data: bytes):
+    ref, ref_payload = oracle.utf8_to_utf16le(data)
+    got, payload = transcode_to_bytes(UTF8_TO_UTF16, data, engine="native")
+    assert got.as_tuple() == ref, (len(data), got, ref)
+    assert payload == ref_payload
+    v = validate(UTF8_TO_UTF16, data, engine="native")
+    assert v.as_tuple() == oracle.validate_utf8(data), (len(data), v)
+
+
+def check_u16(data: bytes):
+    ref, ref_payload = oracle.utf16le_to_utf8(data)
+    got, payload = transcode_to_bytes(UTF16_TO_UTF8, data, engine="native")
+    assert got.as_tuple() == ref, (len(data), got, ref)
+    assert payload == ref_payload
+    v = validate(UTF16_TO_UTF8, data, engine="native")
+    assert v.as_tuple() == oracle.validate_utf16le(data), (len(data), v)
+
+
+# ----------------------------------------------------------------- golden
+
+
+def test_golden_utf8_to_utf16(cuda_ok, golden):
+    for case in golden["utf8_to_utf16"]:
+        got, payload = transcode_to_bytes(UTF8_TO_UTF16, case["input_bytes"], engine="native")
+        assert list(got.as_tuple()) == case["outcome"], case["name"]
+        assert payload_matches(case["payload"], payload), case["name"]
+        v = validate(UTF8_TO_UTF16, case["input_bytes"], engine="native")
+        assert list(v.as_tuple()) == case["validate"], case["name"]
+
+
+def test_golden_utf16_to_utf8(cuda_ok, golden):
+    for case in golden["utf16_to_utf8"]:
+        got, payload = transcode_to_bytes(UTF16_TO_UTF8, case["input_bytes"], engine="native")
+        assert list(got.as_tuple()) == case["outcome"], case["name"]
+        assert payload_matches(case["payload"], payload), case["name"]
+        v = validate(UTF16_TO_UTF8, case["input_bytes"], engine="native")
+        assert list(v.as_tuple()) == case["validate"], case["name"]
+
+
+def test_empty_and_odd(cuda_ok):
+    for d in (UTF8_TO_UTF16, UTF16_TO_UTF8):
+        got, payload = transcode_to_bytes(d, b"", engine="native")
+        assert got.as_tuple() == ("ok", 0, 0) and payload == b""
+        assert validate(d, b"", engine="native").as_tuple() == ("ok", 0, 0)
+    with pytest.raises(ValueError):
+        transcode_to_bytes(UTF16_TO_UTF8, b"\x41", engine="native")
+    with pytest.raises(ValueError):
+        validate(UTF16_TO_UTF8, b"\x00\x41\xff", engine="native")
+
+
+# --------------------------------------------------------------- fuzzing
+
+INTERESTING = list(range(0x80, 0x100)) + [0x00, 0x20, 0x41, 0x7F]
+
+
+def test_random_short_buffers(cuda_ok):
+    rng = random.Random(1234)
+    for k in range(1500):
+        n = rng.randrange(0, 200)
+        pool = INTERESTING if k % 2 else range(256)
+        check_u8(bytes(rng.choice(pool) for _ in range(n)))
+    soup = [0xD800, 0xDBFF, 0xDC00, 0xDFFF, 0xD835, 0xDCAA, 0x41, 0xE9, 0x4E2D, 0xFFFF, 0x7F, 0x80, 0x7FF, 0x800]
+    for k in range(1500):
+        n = rng.randrange(0, 150)
+        words = [rng.choice(soup) if k % 2 else rng.randrange(0x10000) for _ in range(n)]
+        check_u16(words_to_bytes(words))
+
+
+@given(st.binary(max_size=300))
+@settings(max_examples=300, deadline=None)
+def test_hypothesis_utf8(cuda_ok, data):
+    check_u8(data)
+
+
+@given(st.lists(st.integers(0, 0xFFFF), max_size=200))
+@settings(max_examples=300, deadline=None)
+def test_hypothesis_utf16(cuda_ok, words):
+    check_u16(words_to_bytes(words))
+
+
+@given(st.text(max_size=400))
+@settings(max_examples=300, deadline=None)
+def test_hypothesis_valid_text_round_trip(cuda_ok, text):
+    u8 = text.encode("utf-8")
+    got, u16 = transcode_to_bytes(UTF8_TO_UTF16, u8, engine="native")
+    assert got.ok and u16 == text.encode("utf-16-le")
+    got, back = transcode_to_bytes(UTF16_TO_UTF8, u16, engine="native")
+    assert got.ok and back == u8
+
+
+# ------------------------------------------------ tile / warp boundaries
+
+
+def _boundary_positions(n):
+    pos = set()
+    for b in list(range(0, n, 2048)) + list(range(0, min(n, 4096), 128)):
+        for d in range(-5, 6):
+            if 0 <= b + d < n:
+                pos.add(b + d)
+    return sorted(pos)
+
+
+def test_utf8_errors_at_boundaries(cuda_ok):
+    base = corpus.generate("mix", 3 * TILE + 777, seed=21).numpy()
+    rng = random.Random(7)
+    patterns = [b"\x80", b"\xc0", b"\xc1\xbf", b"\xe0\x80\x80", b"\xed\xa0\x80", b"\xf0\x8f\xbf\xbf",
+                b"\xf4\x90\x80\x80", b"\xf5", b"\xff", b"\xe2\x28", b"\xc2", b"\xf0\x9f\x98"]
+    for p in _boundary_positions(len(base)):
+        pat = rng.choice(patterns)
+        data = base.copy()
+        data[p : p + len(pat)] = np.frombuffer(pat, dtype=np.uint8)[: len(data) - p]
+        check_u8(data.tobytes())
+    # truncation exactly at the end of the input, every tail length
+    for cut in range(1, 40):
+        check_u8(base[: len(base) - cut].tobytes())
+
+
+def test_utf16_errors_at_boundaries(cuda_ok):
+    base = corpus.generate("emoji", (3 * TILE + 778) // 2, seed=22, utf16=True).numpy()
+    words = base.view(np.uint16)
+    for p in _boundary_positions(len(words)):
+        for w in (0xD800, 0xDC00, 0xDBFF):
+            data = words.copy()
+            data[p] = w
+            check_u16(data.tobytes())
+    for cut in range(1, 10):
+        check_u16(words[: len(words) - cut].tobytes())
+
+
+def test_every_lead_and_misalignment(cuda_ok):
+    """Input / output pointers at every offset inside a 16-byte granule."""
+    dev = torch.device("cuda", 0)
+    text = corpus.generate("mix", 3 * TILE + 100, seed=23).numpy().tobytes()
+    ref, ref_payload = oracle.utf8_to_utf16le(text)
+    big = torch.zeros(len(text) + 64, dtype=torch.uint8, device=dev)
+    for lead in range(16):
+        big[lead : lead + len(text)] = torch.frombuffer(bytearray(text), dtype=torch.uint8).to(dev)
+        src = big[lead : lead + len(text)]
+        out_big = torch.full((2 * len(text) + 64,), 0xEE, dtype=torch.uint8, device=dev)
+        for olead in (0, 2, 6, 14):
+            out = out_big[olead : olead + 2 * len(text)].view(torch.uint16)
+            res, _ = transcode_device(UTF8_TO_UTF16, src, out)
+            got = outcome_from_tensor(res.cpu())
+            assert got.as_tuple() == ref, (lead, olead)
+            assert out.view(torch.uint8)[: 2 * got.written].cpu().numpy().tobytes() == ref_payload
+        v = outcome_from_tensor(validate_device(UTF8_TO_UTF16, src).cpu())
+        assert v.as_tuple() == oracle.validate_utf8(text)
+    # UTF-16 input at every even lead
+    u16 = text.decode("utf-8").encode("utf-16-le")
+    ref16, ref16_payload = oracle.utf16le_to_utf8(u16)
+    big = torch.zeros(len(u16) + 64, dtype=torch.uint8, device=dev)
+    for lead in range(0, 16, 2):
+        big[lead : lead + len(u16)] = torch.frombuffer(bytearray(u16), dtype=torch.uint8).to(dev)
+        src = big[lead : lead + len(u16)]
+        for olead in (0, 1, 5, 15):
+            out_big = torch.full((3 * len(u16) // 2 + 64,), 0xEE, dtype=torch.uint8, device=dev)
+            out = out_big[olead : olead + 3 * len(u16) // 2]
+            res, _ = transcode_device(UTF16_TO_UTF8, src, out)
+            got = outcome_from_tensor(res.cpu())
+            assert got.as_tuple() == ref16, (lead, olead)
+            assert out[: got.written].cpu().numpy().tobytes() == ref16_payload
+
+
+def test_canary_no_write_past_written(cuda_ok):
+    dev = torch.device("cuda", 0)
+    base = corpus.generate("mix", 2 * TILE + 300, seed=24).numpy()
+    for p in (0, 1, 100, TILE - 1, TILE + 3, 2 * TILE + 200):
+        data = base.copy()
+        data[p] = 0xFF
+        src = torch.from_numpy(data).to(dev)
+        out = torch.full((2 * len(data) + 32,), 0xA5, dtype=torch.uint8, device=dev)
+        res, _ = transcode_device(UTF8_TO_UTF16, src, out[: 2 * len(data)].view(torch.uint16))
+        got = outcome_from_tensor(res.cpu())
+        ref, ref_payload = oracle.utf8_to_utf16le(data.tobytes())
+        assert got.as_tuple() == ref
+        host = out.cpu().numpy()
+        assert host[: 2 * got.written].tobytes() == ref_payload
+        assert (host[2 * got.written :] == 0xA5).all(), p
+    # host bytearray out: only the prefix is written
+    data = base.copy()
+    data[5000] = 0x80
+    buf = bytearray(b"\xee" * (2 * len(data)))
+    got = transcode(UTF8_TO_UTF16, data.tobytes(), buf, engine="native")
+    assert got.status is TranscodeStatus.MALFORMED_INPUT and got.consumed == 5000
+    assert set(buf[2 * got.written :]) == {0xEE}
+
+
+# ------------------------------------------------------ full-size configs
+
+
+@pytest.mark.parametrize("profile", ["latin", "cyrillic", "cjk", "emoji"])
+def test_config2_config3_full_size(cuda_ok, profile):
+    """256 MiB buffers of each profile, both directions, against the oracle."""
+    dev = torch.device("cuda", 0)
+    n = 256 << 20
+    seed = {"latin": 1, "cyrillic": 2, "cjk": 3, "emoji": 4}[profile]
+    src = corpus.generate(profile, n, seed, device=dev)
+    res, out = transcode_device(UTF8_TO_UTF16, src)
+    got = outcome_from_tensor(res.cpu())
+    host = src.cpu().numpy()
+    ref_words = np.empty(n, dtype=np.uint16)
+    ref = oracle.run_mt(oracle.OP_U8_U16, host, nthreads=16, out=ref_words)
+    assert got.as_tuple() == ref == ("ok", n, ref[2])
+    assert torch.equal(out[: got.written].cpu().view(torch.int16),
+                       torch.from_numpy(ref_words[: got.written].view(np.int16)))
+    # UTF-16 buffer of the same profile, back to UTF-8
+    src16 = corpus.generate(profile, n // 2, seed, utf16=True, device=dev)
+    res, out8 = transcode_device(UTF16_TO_UTF8, src16)
+    got = outcome_from_tensor(res.cpu())
+    host16 = src16.cpu().numpy()
+    ref_bytes = np.empty(3 * (n // 2), dtype=np.uint8)
+    ref = oracle.run_mt(oracle.OP_U16_U8, host16, nthreads=16, out=ref_bytes)
+    assert got.as_tuple() == ref
+    assert torch.equal(out8[: got.written].cpu(), torch.from_numpy(ref_bytes[: got.written]))
+
+
+def test_config1_round_trip(cuda_ok):
+    dev = torch.device("cuda", 0)
+    src = corpus.generate("mix", 4 << 20, 0, device=dev)
+    res, words = transcode_device(UTF8_TO_UTF16, src)
+    got = outcome_from_tensor(res.cpu())
+    ref, ref_payload = oracle.utf8_to_utf16le(src.cpu().numpy())
+    assert got.as_tuple() == ref and got.ok
+    assert words[: got.written].cpu().numpy().tobytes() == ref_payload
+    res, back = transcode_device(UTF16_TO_UTF8, words[: got.written])
+    got2 = outcome_from_tensor(res.cpu())
+    assert got2.as_tuple() == ("ok", got.written, 4 << 20)
+    assert torch.equal(back[: 4 << 20], src)
+
+
+@pytest.mark.parametrize("utf16", [False, True])
+def test_config4_error_injection(cuda_ok, utf16):
+    """256 MiB, errors at 1e-6/unit: validate + transcode vs the oracle, plus
+    a zero-error control buffer."""
+    dev = torch.device("cuda", 0)
+    profile = "emoji" if utf16 else "cjk"
+    units = (256 << 20) // 2 if utf16 else 256 << 20
+    src = corpus.generate(profile, units, 3 if not utf16 else 4, utf16=utf16, device=dev)
+    direction = UTF16_TO_UTF8 if utf16 else UTF8_TO_UTF16
+    # control
+    v = outcome_from_tensor(validate_device(direction, src).cpu())
+    assert v.as_tuple() == ("ok", units, 0)
+    planted = corpus.inject_errors(src, utf16=utf16, rate=1e-6, seed=101 + int(utf16))
+    assert len(planted) > 10
+    host = src.cpu().numpy()
+    ref_v = oracle.run_mt(oracle.OP_VAL_U16 if utf16 else oracle.OP_VAL_U8, host, nthreads=16)
+    v = outcome_from_tensor(validate_device(direction, src).cpu())
+    assert v.as_tuple() == ref_v and ref_v[0] == "malformed-input"
+    assert ref_v[1] == min(p for p, _ in planted) or ref_v[1] <= min(p for p, _ in planted)
+    res, out = transcode_device(direction, src)
+    got = outcome_from_tensor(res.cpu())
+    if utf16:
+        ref_out = np.empty(3 * units, dtype=np.uint8)
+        ref = oracle.run_mt(oracle.OP_U16_U8, host, nthreads=16, out=ref_out)
+        assert got.as_tuple() == ref
+        assert out[: got.written].cpu().numpy().tobytes() == ref_out[: got.written].tobytes()
+    else:
+        ref_out = np.empty(units, dtype=np.uint16)
+        ref = oracle.run_mt(oracle.OP_U8_U16, host, nthreads=16, out=ref_out)
+        assert got.as_tuple() == ref
+        assert out[: got.written].cpu().numpy().tobytes() == ref_out[: got.written].tobytes()
+
+
+@pytest.mark.parametrize("kind", corpus.UTF8_ERROR_KINDS)
+def test_each_utf8_error_kind(cuda_ok, kind):
+    base = corpus.generate("cjk", 200_000, seed=9).numpy()
+    for s in range(20):
+        data = torch.from_numpy(base.copy())
+        corpus.inject_errors(data, utf16=False, rate=2e-5, seed=500 + s, kinds=(kind,))
+        check_u8(data.numpy().tobytes())
+
+
+@pytest.mark.parametrize("kind", corpus.UTF16_ERROR_KINDS)
+def test_each_utf16_error_kind(cuda_ok, kind):
+    base = corpus.generate("emoji", 100_000, seed=9, utf16=True).numpy()
+    for s in range(20):
+        data = torch.from_numpy(base.copy())
+        corpus.inject_errors(data, utf16=True, rate=2e-5, seed=600 + s, kinds=(kind,))
+        check_u16(data.numpy().tobytes())
