@@ -1,0 +1,440 @@
+"""Benchmark: validating UTF-8 -> UTF-16LE transcode on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Headline workload (config 2 of BASELINE.json): four 256 MiB valid UTF-8
+buffers, one per seeded profile (latin, cyrillic, cjk, emoji; seeds 1-4),
+generated directly in HBM.  One step = one validating transcode of all four
+buffers.  ``value`` = input GiB/s over the whole job (device-timed with CUDA
+events on the launch stream, inputs resident in HBM, max over ranks).
+Every buffer is larger than the 126 MB L2, so no L2 flush is needed between
+steps.  ``e2e`` repeats the step through the public facade with pinned host
+buffers (H2D of the input, D2H of the outcome and of the written payload
+inside the timed region).  Extra keys carry config 3 (UTF-16LE -> UTF-8) and
+config 4 (validate) numbers measured in the same run.
+
+Multi-GPU (torchrun, one rank per GPU): every rank transcodes its own four
+buffers (weak scaling) and the per-shard outcomes are exchanged each step
+with one NCCL all_gather of int64[3] per buffer -- the only data-path
+collective of the sharded design.
+
+``--impl reference`` times the reference algorithm's CPU restatement
+(oracle/, C, all host threads, character-boundary sharded) on the same
+workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PROFILES = (("latin", 1), ("cyrillic", 2), ("cjk", 3), ("emoji", 4))
+BUF_BYTES = 256 << 20
+METRIC = "input GiB/s transcoded+validated (device-timed) and % of HBM roofline"
+GIB = float(1 << 30)
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md, 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per input byte of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle",
+        0x2: "applications_clocks_setting",
+        0x4: "sw_power_cap",
+        0x8: "hw_slowdown",
+        0x10: "sync_boost",
+        0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML missing
+            self._nvml = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self._nvml.nvmlDeviceGetClockInfo(self._h, self._nvml.NVML_CLOCK_SM))
+                bits = self._nvml.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for b, name in self.REASONS.items():
+                    if bits & b and b != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._nvml is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self._nvml is not None:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "reasons": sorted(self.reasons),
+            "samples": len(self.samples),
+        }
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (C restatement of
+    laneutf.scalar) on all host threads, same workload, rank 0 only."""
+    import oracle
+
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2212_05098_b200 import corpus
+
+    gen_dev = "cuda" if torch.cuda.is_available() else "cpu"
+    bufs = [corpus.generate(p, BUF_BYTES, s, device=gen_dev).cpu().numpy() for p, s in PROFILES]
+    outs = [np.empty(BUF_BYTES, dtype=np.uint16) for _ in bufs]
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        for b, o in zip(bufs, outs):
+            oracle.run_mt(oracle.OP_U8_U16, b, threads, o)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for b, o in zip(bufs, outs):
+            res = oracle.run_mt(oracle.OP_U8_U16, b, threads, o)
+            assert res[0] == "ok"
+    dt = time.perf_counter() - t0
+    value = args.steps * len(bufs) * BUF_BYTES / GIB / dt
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "GiB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(1e3 * dt / args.steps, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic (seeded SplitMix64 profiles, corpus.py)",
+        "config": {
+            "workload": "config2: UTF-8->UTF-16LE, 4 x 256 MiB profiles (latin/cyrillic/cjk/emoji, seeds 1-4)",
+            "input_bytes_per_step": len(bufs) * BUF_BYTES,
+        },
+        "cpu_baseline": {
+            "value": round(value, 3),
+            "unit": "GiB/s",
+            "cores": threads,
+            "kind": "port",
+            "sample": "full config-2 workload per step (4 x 256 MiB), oracle/laneutf_oracle.c "
+            "(C restatement of laneutf.scalar), character-boundary sharded over host threads",
+        },
+        "e2e": {"value": round(value, 3), "unit": "GiB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample():
+    """Oracle on a bounded sample of the same workload (rank 0, N=1)."""
+    import oracle
+
+    from paper_2212_05098_b200 import corpus
+
+    sample = 64 << 20
+    bufs = [corpus.generate(p, sample, s, device="cuda").cpu().numpy() for p, s in PROFILES]
+    outs = [np.empty(sample, dtype=np.uint16) for _ in bufs]
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    for b, o in zip(bufs, outs):
+        oracle.run_mt(oracle.OP_U8_U16, b, threads, o)
+    dt_mt = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.run_mt(oracle.OP_U8_U16, bufs[2][: 16 << 20], 1, outs[2])
+    dt_1 = time.perf_counter() - t0
+    return {
+        "value": round(len(bufs) * sample / GIB / dt_mt, 3),
+        "unit": "GiB/s",
+        "cores": threads,
+        "kind": "port",
+        "sample": f"first 64 MiB of each config-2 profile buffer (256 MiB), oracle/laneutf_oracle.c "
+        f"on {threads} host threads; single-thread cjk 16 MiB = {16 / 1024 / dt_1:.3f} GiB/s",
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-extras", action="store_true", help="skip config 3/4 side measurements")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch.distributed as dist
+
+    from paper_2212_05098_b200 import (
+        UTF8_TO_UTF16,
+        UTF16_TO_UTF8,
+        corpus,
+        outcome_from_tensor,
+        transcode,
+        transcode_device,
+        validate_device,
+    )
+    from paper_2212_05098_b200 import _native
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    reason = _native.unavailable_reason(local)
+    if reason is not None:
+        raise SystemExit(f"native engine unavailable: {reason}")
+
+    # ---- inputs resident in HBM (each rank: its own seeded shard of profiles)
+    srcs = [corpus.generate(p, BUF_BYTES, s + 100 * rank, device=dev) for p, s in PROFILES]
+    outs = [torch.empty(BUF_BYTES, dtype=torch.uint16, device=dev) for _ in srcs]
+    ress = [torch.empty(3, dtype=torch.int64, device=dev) for _ in srcs]
+    wss = [
+        torch.empty(_native.workspace_bytes(_native.OP_UTF8_TO_UTF16LE, BUF_BYTES) // 8 + 1, dtype=torch.int64,
+                    device=dev)
+        for _ in srcs
+    ]
+    gathered = [torch.empty(3 * world, dtype=torch.int64, device=dev) for _ in srcs]
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        for i, (s, o, r, w) in enumerate(zip(srcs, outs, ress, wss)):
+            if ev is not None:
+                ev[i][0].record(stream)
+            transcode_device(UTF8_TO_UTF16, s, o, res=r, ws=w, stream=stream)
+            if ev is not None:
+                ev[i][1].record(stream)
+        if world > 1:
+            for r, g in zip(ress, gathered):
+                dist.all_gather_into_tensor(g, r)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    outcomes = [outcome_from_tensor(r.cpu()) for r in ress]
+    assert all(o.ok for o in outcomes), outcomes
+    in_bytes = len(srcs) * BUF_BYTES
+    out_bytes = sum(2 * o.written for o in outcomes)
+
+    # ---- timed region
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in srcs]
+           for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(evs[k])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    per_launch = np.array([[a.elapsed_time(b) for (a, b) in row] for row in evs])  # ms [steps, bufs]
+    if world > 1:
+        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    value = world * args.steps * in_bytes / GIB / (elapsed_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (k_utf8_to_utf16le)
+    peak, peak_src = measured_peak()
+    alg_bytes = np.array([BUF_BYTES + 2 * o.written for o in outcomes], dtype=np.float64)
+    mean_launch_s = per_launch.mean(axis=0) / 1e3
+    achieved = float((alg_bytes / mean_launch_s).mean() / 1e9)
+    prof_detail = {}
+    for (p, _), o, ab, t in zip(PROFILES, outcomes, alg_bytes, mean_launch_s):
+        prof_detail[p] = {
+            "input_gib_s": round(BUF_BYTES / GIB / t, 2),
+            "alg_gb_s": round(ab / t / 1e9, 1),
+            "frac_of_measured": round(ab / t / 1e9 / peak, 4),
+            "frac_of_8tbs": round(ab / t / 1e9 / 8000.0, 4),
+            "us_per_launch": round(t * 1e6, 2),
+            "written_words": o.written,
+        }
+    ncu = ncu_traffic()
+    traffic = None
+    if ncu and "k_utf8_to_utf16le" in ncu:
+        traffic = ncu["k_utf8_to_utf16le"].get("dram_bytes_per_launch")
+
+    line = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "GiB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(elapsed_ms / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8",
+        "data": "synthetic (seeded SplitMix64 profiles generated in HBM, corpus.py)",
+        "config": {
+            "workload": "config2: UTF-8->UTF-16LE, 4 x 256 MiB valid buffers per GPU "
+            "(latin/cyrillic/cjk/emoji, seeds 1-4 (+100*rank))",
+            "input_bytes_per_step": in_bytes,
+            "output_bytes_per_step": out_bytes,
+            "l2": "inputs larger than L2 (256 MiB each > 126 MB), no flush",
+            "parallelism": f"dp{world} (independent shards, NCCL all_gather of outcomes)" if world > 1 else "dp1",
+        },
+        "roofline": {
+            "bound": "hbm",
+            "achieved": round(achieved, 1),
+            "peak": peak,
+            "unit": "GB/s",
+            "frac": round(achieved / peak, 4),
+            "traffic": traffic,
+            "kernel": "k_utf8_to_utf16le",
+            "algorithmic_bytes": "input bytes + 2 x written words, per launch",
+            "peak_source": peak_src,
+            "per_profile": prof_detail,
+        },
+        "gpu_launches": args.steps * len(srcs),
+        "clocks": clocks.summary(),
+    }
+
+    # ---- e2e through the public facade with pinned host buffers
+    hosts = [s.cpu().pin_memory() for s in srcs]
+    host_outs = [torch.empty(2 * BUF_BYTES, dtype=torch.uint8).pin_memory() for _ in srcs]
+    for h, ho in zip(hosts, host_outs):
+        transcode(UTF8_TO_UTF16, h, ho, engine="native")
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        for h, ho in zip(hosts, host_outs):
+            o = transcode(UTF8_TO_UTF16, h, ho, engine="native")
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    line["e2e"] = {
+        "value": round(world * args.e2e_steps * in_bytes / GIB / e2e_s, 3),
+        "unit": "GiB/s",
+        "h2d_bytes_per_step": in_bytes,
+        "d2h_bytes_per_step": out_bytes + 24 * len(srcs),
+        "steps": args.e2e_steps,
+        "api": "paper_2212_05098_b200.transcode(UTF8_TO_UTF16, pinned_in, pinned_out, engine='native')",
+    }
+    del hosts, host_outs
+
+    # ---- extras: config 3 (UTF-16 -> UTF-8) and config 4 (validate), same run
+    if not args.no_extras:
+        extras = {}
+        k_ex = max(3, min(args.steps, 50))
+        src16 = [corpus.generate(p, BUF_BYTES // 2, s + 100 * rank, utf16=True, device=dev) for p, s in PROFILES]
+        out8 = torch.empty(3 * BUF_BYTES // 2, dtype=torch.uint8, device=dev)
+        c3 = {}
+        for (p, _), s16 in zip(PROFILES, src16):
+            res, _ = transcode_device(UTF16_TO_UTF8, s16, out8)
+            o = outcome_from_tensor(res.cpu())
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(k_ex):
+                transcode_device(UTF16_TO_UTF8, s16, out8, res=res)
+            b.record(stream)
+            torch.cuda.synchronize()
+            t = a.elapsed_time(b) / 1e3 / k_ex
+            ab = BUF_BYTES + o.written
+            c3[p] = {"input_gib_s": round(BUF_BYTES / GIB / t, 2), "frac_of_measured": round(ab / t / 1e9 / peak, 4),
+                     "ok": o.ok}
+        extras["config3_utf16_to_utf8"] = c3
+        c4 = {}
+        for name, direction, buf in (("cjk_utf8", UTF8_TO_UTF16, srcs[2]), ("emoji_utf16", UTF16_TO_UTF8, src16[3])):
+            res = validate_device(direction, buf)
+            o = outcome_from_tensor(res.cpu())
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(k_ex):
+                validate_device(direction, buf, res=res)
+            b.record(stream)
+            torch.cuda.synchronize()
+            t = a.elapsed_time(b) / 1e3 / k_ex
+            c4[name] = {"input_gib_s": round(BUF_BYTES / GIB / t, 2),
+                        "frac_of_measured": round(BUF_BYTES / t / 1e9 / peak, 4), "ok": o.ok,
+                        "control": "zero-error buffer"}
+        extras["config4_validate"] = c4
+        line["extras"] = extras
+
+    if rank == 0 and world == 1:
+        try:
+            line["cpu_baseline"] = cpu_baseline_sample()
+        except Exception as exc:  # the baseline must not sink the GPU line
+            line["cpu_baseline"] = {"value": None, "error": repr(exc)[:200]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
