@@ -24,9 +24,9 @@ constexpr int kOutStrideU16 = kChunkBytes + 16;      // words per warp staging r
 constexpr int kOutStrideU8 = 3 * kChunkBytes / 2 + 32; // bytes per warp region (<= 3 bytes per word)
 
 constexpr size_t kInSmemBytes = sizeof(uint32_t) * kInWords;
-constexpr size_t kSmemK1 = kInSmemBytes + sizeof(uint16_t) * kOutStrideU16 * kWarps;
+constexpr size_t kSmemK1 = 2 * sizeof(uint16_t) * kOutStrideU16 * kWarps; // double-buffered staging
 constexpr size_t kSmemK2 = kInSmemBytes + kOutStrideU8 * kWarps;
-constexpr size_t kSmemVal = kInSmemBytes;
+constexpr size_t kSmemVal = kInSmemBytes; // K4 (UTF-16) stages its tile; K3 reads registers
 
 struct TileShared {
     WarpResult wres[kWarps];
@@ -39,76 +39,86 @@ struct TileShared {
 
 // ------------------------------------------------------------- copy-out
 
-// Copy cnt UTF-16 words from shared memory (16-byte aligned region) to the
-// output at word index g0 of the 16-byte aligned frame out_a (so 16-byte
-// chunks are aligned); partial head/tail chunks go word by word.
+// Copy cnt UTF-16 words from a warp's shared staging region (16-byte aligned)
+// to out_a[g0 ..) (out_a 16-byte aligned).  Interior 16-byte chunks use vector
+// stores; the partial head/tail chunks are written word-parallel by lanes
+// 0..15.  All index math is 32-bit relative to the aligned chunk start.
 __device__ __forceinline__ void copy_out_u16(const uint16_t *src, uint32_t cnt, uint16_t *out_a, uint64_t g0)
 {
     if (cnt == 0)
         return;
     const uint32_t lane = lane_id();
-    const uint64_t g_end = g0 + cnt;
-    const uint64_t a0 = g0 & ~7ull;
-    const uint32_t shift = (uint32_t)(g0 - a0);
-    const uint32_t nchunks = (uint32_t)((g_end - a0 + 7) >> 3);
+    const uint32_t shift = (uint32_t)(g0 & 7);
+    uint16_t *dst = out_a + (g0 - shift); // 16-byte aligned
+    const uint32_t total = shift + cnt;   // words from the aligned start
+    const uint32_t full_lo = shift ? 1u : 0u, full_hi = total >> 3;
     const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
-    for (uint32_t c = lane; c < nchunks; c += 32) {
-        const uint64_t a = a0 + 8ull * c;
-        const int32_t j = (int32_t)(8 * c) - (int32_t)shift;
-        if (a >= g0 && a + 8 <= g_end) {
-            uint4 v;
-            if ((shift & 1) == 0) {
-                const int m = j >> 1;
-                v = make_uint4(s32[m], s32[m + 1], s32[m + 2], s32[m + 3]);
-            } else {
-                const int m = (j - 1) >> 1;
-                const uint32_t w0 = s32[m], w1 = s32[m + 1], w2 = s32[m + 2], w3 = s32[m + 3], w4 = s32[m + 4];
-                v = make_uint4(prmt(w0, w1, 0x5432), prmt(w1, w2, 0x5432), prmt(w2, w3, 0x5432),
-                               prmt(w3, w4, 0x5432));
-            }
-            __stcs(reinterpret_cast<uint4 *>(out_a + a), v);
-        } else {
-            for (int k = 0; k < 8; ++k) {
-                const uint64_t g = a + k;
-                if (g >= g0 && g < g_end)
-                    out_a[g] = src[j + k];
-            }
+    if (shift == 0) {
+        const uint4 *s128 = reinterpret_cast<const uint4 *>(src);
+        for (uint32_t c = full_lo + lane; c < full_hi; c += 32)
+            __stcs(reinterpret_cast<uint4 *>(dst) + c, s128[c]);
+    } else if ((shift & 1) == 0) {
+        for (uint32_t c = full_lo + lane; c < full_hi; c += 32) {
+            const uint32_t m = (8 * c - shift) >> 1;
+            __stcs(reinterpret_cast<uint4 *>(dst) + c, make_uint4(s32[m], s32[m + 1], s32[m + 2], s32[m + 3]));
+        }
+    } else {
+        for (uint32_t c = full_lo + lane; c < full_hi; c += 32) {
+            const uint32_t m = (8 * c - shift - 1) >> 1;
+            const uint32_t w0 = s32[m], w1 = s32[m + 1], w2 = s32[m + 2], w3 = s32[m + 3], w4 = s32[m + 4];
+            __stcs(reinterpret_cast<uint4 *>(dst) + c, make_uint4(prmt(w0, w1, 0x5432), prmt(w1, w2, 0x5432),
+                                                                  prmt(w2, w3, 0x5432), prmt(w3, w4, 0x5432)));
+        }
+    }
+    // partial chunks: head (chunk 0 when shift > 0) and tail (chunk full_hi)
+    if (lane < 16) {
+        uint32_t chunk;
+        if (lane < 8)
+            chunk = shift ? 0u : 0xffffffffu;
+        else
+            chunk = (total & 7) && !(shift && full_hi == 0) ? full_hi : 0xffffffffu;
+        if (chunk != 0xffffffffu) {
+            const uint32_t i = 8 * chunk + (lane & 7);
+            if (i >= shift && i < total)
+                dst[i] = src[i - shift];
         }
     }
 }
 
-// Same for bytes (UTF-8 output), 16-byte chunks.
+// Same for bytes (UTF-8 output), 16-byte chunks; head/tail by lanes 0..31.
 __device__ __forceinline__ void copy_out_u8(const uint8_t *src, uint32_t cnt, uint8_t *out_a, uint64_t g0)
 {
     if (cnt == 0)
         return;
     const uint32_t lane = lane_id();
-    const uint64_t g_end = g0 + cnt;
-    const uint64_t a0 = g0 & ~15ull;
-    const uint32_t shift = (uint32_t)(g0 - a0);
-    const uint32_t nchunks = (uint32_t)((g_end - a0 + 15) >> 4);
+    const uint32_t shift = (uint32_t)(g0 & 15);
+    uint8_t *dst = out_a + (g0 - shift);
+    const uint32_t total = shift + cnt;
+    const uint32_t full_lo = shift ? 1u : 0u, full_hi = total >> 4;
     const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
-    const uint32_t sh = 8u * ((16u - shift) & 3u); // byte shift inside the smem word
-    for (uint32_t c = lane; c < nchunks; c += 32) {
-        const uint64_t a = a0 + 16ull * c;
-        const int32_t j = (int32_t)(16 * c) - (int32_t)shift;
-        if (a >= g0 && a + 16 <= g_end) {
-            const int m = j >> 2; // floor (j >= 0 here)
-            uint4 v;
-            if (sh == 0) {
-                v = make_uint4(s32[m], s32[m + 1], s32[m + 2], s32[m + 3]);
-            } else {
-                const uint32_t w0 = s32[m], w1 = s32[m + 1], w2 = s32[m + 2], w3 = s32[m + 3], w4 = s32[m + 4];
-                v = make_uint4(fsr(w0, w1, sh), fsr(w1, w2, sh), fsr(w2, w3, sh), fsr(w3, w4, sh));
-            }
-            __stcs(reinterpret_cast<uint4 *>(out_a + a), v);
-        } else {
-            for (int k = 0; k < 16; ++k) {
-                const uint64_t g = a + k;
-                if (g >= g0 && g < g_end)
-                    out_a[g] = src[j + k];
-            }
+    const uint32_t sh = 8u * ((16u - shift) & 3u);
+    if (sh == 0) {
+        for (uint32_t c = full_lo + lane; c < full_hi; c += 32) {
+            const uint32_t m = (16 * c - shift) >> 2;
+            __stcs(reinterpret_cast<uint4 *>(dst) + c, make_uint4(s32[m], s32[m + 1], s32[m + 2], s32[m + 3]));
         }
+    } else {
+        for (uint32_t c = full_lo + lane; c < full_hi; c += 32) {
+            const uint32_t m = (16 * c - shift) >> 2;
+            const uint32_t w0 = s32[m], w1 = s32[m + 1], w2 = s32[m + 2], w3 = s32[m + 3], w4 = s32[m + 4];
+            __stcs(reinterpret_cast<uint4 *>(dst) + c,
+                   make_uint4(fsr(w0, w1, sh), fsr(w1, w2, sh), fsr(w2, w3, sh), fsr(w3, w4, sh)));
+        }
+    }
+    uint32_t chunk;
+    if (lane < 16)
+        chunk = shift ? 0u : 0xffffffffu;
+    else
+        chunk = (total & 15) && !(shift && full_hi == 0) ? full_hi : 0xffffffffu;
+    if (chunk != 0xffffffffu) {
+        const uint32_t i = 16 * chunk + (lane & 15);
+        if (i >= shift && i < total)
+            dst[i] = src[i - shift];
     }
 }
 
@@ -158,55 +168,160 @@ __device__ __forceinline__ void sel_table_init(SelPair *sel)
     }
 }
 
+// ====================================================== pipelined transcode
+//
+// Persistent CTAs (grid = resident capacity), each walking tiles
+// blockIdx.x, blockIdx.x + gridDim.x, ...  Warps 0..7 compute a tile into one
+// of two staging buffers; warp 8 is the look-back warp: it combines the warp
+// results, publishes the tile aggregate, resolves the exclusive prefix and
+// hands it back through a named barrier.  Meanwhile the compute warps already
+// work on the next tile, and only copy a tile out once its prefix is known,
+// so look-back latency overlaps compute instead of idling the CTA.
+//
+// Named barriers: 1+b "tile in buffer b computed" (compute warps arrive, the
+// look-back warp syncs); 3+b "prefix of buffer b known" (look-back warp
+// arrives, compute warps sync).  Every CTA is resident, and a tile only waits
+// on smaller tile indices, so progress is guaranteed.
+
+constexpr int kPipeThreads = kThreads + 32;
+
+struct PipeShared {
+    WarpResult wres[2][kWarps];
+    uint32_t warp_excl[2][kWarps];
+    uint64_t excl[2];
+    uint32_t first_err[2];
+    uint32_t ticket[2];  // tile claimed for iteration i lives in ticket[i & 1]
+    uint32_t tile_of[2]; // tile held by each staging buffer (0xffffffff: stop)
+};
+
+__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint32_t id, uint32_t n)
+{
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Look-back warp body for one tile; unit_shift = 0 for byte positions (UTF-8
+// input), 1 for word positions (UTF-16 input).
+__device__ __forceinline__ void pipe_lookback(PipeShared &ps, uint32_t buf, uint32_t tile, uint64_t *status,
+                                              Outcome *res, uint32_t ntiles, int64_t lo_b, uint64_t n_units,
+                                              int unit_shift)
+{
+    const uint32_t lane = lane_id();
+    uint32_t first = kWarps, units = 0;
+    if (lane == 0) {
+        for (int w = 0; w < kWarps; ++w) {
+            ps.warp_excl[buf][w] = units;
+            units += ps.wres[buf][w].units;
+            if (ps.wres[buf][w].err) {
+                first = (uint32_t)w;
+                break;
+            }
+        }
+        ps.first_err[buf] = first;
+    }
+    first = __shfl_sync(0xffffffffu, first, 0);
+    units = __shfl_sync(0xffffffffu, units, 0);
+    const uint64_t agg = (first < kWarps ? kErrBit : 0ull) | (uint64_t)units;
+    const uint64_t ex = lookback(status, tile, agg);
+    if (lane == 0) {
+        ps.excl[buf] = ex;
+        if (!(ex & kErrBit)) {
+            const uint64_t written = (ex & kValMask) + units;
+            const int64_t tile_off = (int64_t)tile * kTileBytes;
+            if (first < kWarps) {
+                res->status = kStatusMalformed;
+                res->pad = 0;
+                res->consumed = (uint64_t)((tile_off + ps.wres[buf][first].pos - lo_b) >> unit_shift);
+                res->written = written;
+            } else if (tile == ntiles - 1) {
+                res->status = kStatusOk;
+                res->pad = 0;
+                res->consumed = n_units;
+                res->written = written;
+            }
+        }
+    }
+}
+
 // ===================================================================== K1
 
-__global__ void __launch_bounds__(kThreads) k_utf8_to_utf16le(const uint8_t *__restrict__ base, uint32_t lead,
-                                                               uint64_t n, uint16_t *__restrict__ out_a,
-                                                               uint32_t out_lead_words, uint64_t *__restrict__ status,
-                                                               Outcome *__restrict__ res, uint32_t ntiles)
+__global__ void __launch_bounds__(kPipeThreads, 3)
+    k_utf8_to_utf16le(const uint8_t *__restrict__ base, uint32_t lead, uint64_t n, uint16_t *__restrict__ out_a,
+                      uint32_t out_lead_words, uint64_t *__restrict__ status, Outcome *__restrict__ res,
+                      uint32_t ntiles)
 {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    uint32_t *in_s = reinterpret_cast<uint32_t *>(smem_raw);
-    uint16_t *out_s = reinterpret_cast<uint16_t *>(smem_raw + kInSmemBytes);
+    uint16_t *out_s = reinterpret_cast<uint16_t *>(smem_raw); // [2][kWarps][kOutStrideU16]
     __shared__ SelPair sel[16];
-    __shared__ TileShared ts;
+    __shared__ PipeShared ps;
 
-    const int64_t tile_off = (int64_t)blockIdx.x * kTileBytes;
     const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n;
-    const bool interior = stage_tile(in_s, base, tile_off, lo_b, hi_b);
+    unsigned int *ticket = reinterpret_cast<unsigned int *>(status + ntiles);
     sel_table_init(sel);
+    if (threadIdx.x == 0)
+        ps.ticket[0] = atomicAdd(ticket, 1u);
     __syncthreads();
-
     const uint32_t warp = threadIdx.x >> 5;
-    uint16_t *out_w = out_s + warp * kOutStrideU16;
-    if (interior)
-        u8u16_warp<false>(in_s, out_w, sel, tile_off, lo_b, hi_b, ts.wres[warp]);
-    else
-        u8u16_warp<true>(in_s, out_w, sel, tile_off, lo_b, hi_b, ts.wres[warp]);
-    __syncthreads();
-    tile_scan(ts, status);
 
-    const uint64_t ex = ts.excl;
-    if (ex & kErrBit)
-        return; // an earlier tile holds the first error: nothing here is output
-    const uint32_t first = ts.first_err_warp;
-    if (warp <= first && warp < kWarps) {
-        const uint64_t g0 = (ex & kValMask) + ts.warp_excl[warp] + out_lead_words;
-        copy_out_u16(out_w, ts.wres[warp].units, out_a, g0);
-    }
-    if (threadIdx.x == 0) {
-        const uint64_t written = (ex & kValMask) + ts.tile_units;
-        if (first < kWarps) {
-            res->status = kStatusMalformed;
-            res->pad = 0;
-            res->consumed = (uint64_t)(tile_off + ts.wres[first].pos - lo_b);
-            res->written = written;
-        } else if (blockIdx.x == ntiles - 1) {
-            res->status = kStatusOk;
-            res->pad = 0;
-            res->consumed = n;
-            res->written = written;
+    if (warp == kWarps) {
+        for (uint32_t i = 0;; ++i) {
+            const uint32_t buf = i & 1;
+            bar_sync(1 + buf, kPipeThreads);
+            const uint32_t tile = ps.tile_of[buf];
+            if (tile >= ntiles)
+                break; // sentinel: the compute warps ran out of tiles
+            pipe_lookback(ps, buf, tile, status, res, ntiles, lo_b, n, 0);
+            bar_arrive(3 + buf, kPipeThreads);
         }
+        return;
+    }
+
+    // Tiles are claimed just before they are computed (ticket order ==
+    // compute order), so a tile's look-back only waits on tiles that started
+    // earlier.
+    uint32_t i = 0;
+    for (;; ++i) {
+        const uint32_t buf = i & 1;
+        const uint32_t tile = ps.ticket[buf];
+        if (tile >= ntiles) {
+            if (threadIdx.x == 0)
+                ps.tile_of[buf] = 0xffffffffu;
+            bar_arrive(1 + buf, kPipeThreads);
+            break;
+        }
+        const int64_t tile_off = (int64_t)tile * kTileBytes;
+        uint16_t *out_w = out_s + (buf * kWarps + warp) * kOutStrideU16;
+        const bool interior = (tile_off - 4 >= lo_b) && (tile_off + kTileBytes + 4 <= hi_b);
+        if (interior)
+            u8u16_warp<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][warp]);
+        else
+            u8u16_warp<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][warp]);
+        if (threadIdx.x == 0)
+            ps.tile_of[buf] = tile;
+        bar_arrive(1 + buf, kPipeThreads);
+        if (threadIdx.x == 0)
+            ps.ticket[buf ^ 1] = atomicAdd(ticket, 1u); // next tile, claimed now
+        if (i == 0)
+            bar_sync(5, kThreads); // publish ps.ticket[1] to the compute warps
+        if (i > 0) {
+            const uint32_t pb = buf ^ 1;
+            bar_sync(3 + pb, kPipeThreads);
+            const uint64_t ex = ps.excl[pb];
+            if (!(ex & kErrBit) && warp <= ps.first_err[pb])
+                copy_out_u16(out_s + (pb * kWarps + warp) * kOutStrideU16, ps.wres[pb][warp].units, out_a,
+                             (ex & kValMask) + ps.warp_excl[pb][warp] + out_lead_words);
+        }
+    }
+    if (i > 0) {
+        const uint32_t pb = (i - 1) & 1;
+        bar_sync(3 + pb, kPipeThreads);
+        const uint64_t ex = ps.excl[pb];
+        if (!(ex & kErrBit) && warp <= ps.first_err[pb])
+            copy_out_u16(out_s + (pb * kWarps + warp) * kOutStrideU16, ps.wres[pb][warp].units, out_a,
+                         (ex & kValMask) + ps.warp_excl[pb][warp] + out_lead_words);
     }
 }
 
@@ -284,19 +399,20 @@ __global__ void __launch_bounds__(kThreads) k_validate(const uint8_t *__restrict
     }
     __syncthreads();
     if (!ts.skip) {
-        const bool interior = stage_tile(in_s, base, tile_off, lo_b, hi_b);
-        __syncthreads();
         const uint32_t warp = threadIdx.x >> 5;
         if (Utf16) {
+            const bool interior = stage_tile(in_s, base, tile_off, lo_b, hi_b);
+            __syncthreads();
             if (interior)
                 u16val_warp<false>(in_s, tile_off, lo_b, hi_b, ts.wres[warp]);
             else
                 u16val_warp<true>(in_s, tile_off, lo_b, hi_b, ts.wres[warp]);
         } else {
+            const bool interior = (tile_off - 4 >= lo_b) && (tile_off + kTileBytes + 4 <= hi_b);
             if (interior)
-                u8val_warp<false>(in_s, tile_off, lo_b, hi_b, ts.wres[warp]);
+                u8val_warp<false>(base, tile_off, lo_b, hi_b, ts.wres[warp]);
             else
-                u8val_warp<true>(in_s, tile_off, lo_b, hi_b, ts.wres[warp]);
+                u8val_warp<true>(base, tile_off, lo_b, hi_b, ts.wres[warp]);
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -367,6 +483,25 @@ static int set_smem_attrs()
     return 0;
 }
 
+// Grid of a persistent pipelined kernel: every CTA must be resident (tiles
+// wait on smaller tiles held by other CTAs), so never exceed the occupancy.
+static int persistent_grid(const void *fn, int threads, size_t smem, uint64_t ntiles, unsigned *grid)
+{
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess)
+        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "occupancy query");
+    if (per_sm < 1)
+        return fail(LU_ERR_CUDA, "pipelined kernel cannot be resident on this device");
+    const uint64_t cap = (uint64_t)sms * (uint64_t)per_sm;
+    *grid = (unsigned)(ntiles < cap ? ntiles : cap);
+    return 0;
+}
+
 } // namespace lu
 
 using namespace lu;
@@ -415,21 +550,25 @@ int lu_utf8_to_utf16le(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint6
         return fail(LU_ERR_INVALID, "null output");
     const uint32_t lead = (uint32_t)((uintptr_t)in & 15);
     const uint64_t nt = n_tiles(n_bytes, lead);
-    if (ws_bytes < 8 * nt)
+    if (ws_bytes < 8 * (nt + 1)) // tile status words + the tile ticket counter
         return fail(LU_ERR_WORKSPACE, "workspace too small (see lu_workspace_bytes)");
     if (nt > 0x7fffffffull)
         return fail(LU_ERR_INVALID, "input too large");
     int rc = set_smem_attrs();
     if (rc)
         return rc;
-    cudaError_t e = cudaMemsetAsync(ws, 0, 8 * nt, stream);
+    cudaError_t e = cudaMemsetAsync(ws, 0, 8 * (nt + 1), stream);
     if (e != cudaSuccess)
         return cuda_fail(e, "cudaMemsetAsync");
     const uint8_t *base = in ? in - lead : reinterpret_cast<const uint8_t *>(16);
     uint16_t *out_safe = out ? out : reinterpret_cast<uint16_t *>(16);
     const uint32_t out_lead = (uint32_t)(((uintptr_t)out_safe & 15) >> 1);
     uint16_t *out_a = out_safe - out_lead;
-    k_utf8_to_utf16le<<<(unsigned)nt, kThreads, kSmemK1, stream>>>(base, lead, n_bytes, out_a, out_lead,
+    unsigned grid = 0;
+    rc = persistent_grid((const void *)k_utf8_to_utf16le, kPipeThreads, kSmemK1, nt, &grid);
+    if (rc)
+        return rc;
+    k_utf8_to_utf16le<<<grid, kPipeThreads, kSmemK1, stream>>>(base, lead, n_bytes, out_a, out_lead,
                                                                    reinterpret_cast<uint64_t *>(ws),
                                                                    reinterpret_cast<Outcome *>(res), (uint32_t)nt);
     e = cudaGetLastError();

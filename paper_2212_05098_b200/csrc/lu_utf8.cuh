@@ -14,12 +14,15 @@
 //     * it is a lead C2..F4 whose continuations are missing / truncated or
 //       whose second byte is out of range (E0 A0.., ED ..9F, F0 90.., F4 ..8F).
 //
-// Per 4-byte quad the kernels compute SWAR byte masks (bit 7 of each byte):
-// C = continuation, L = >=C0, E = >=E0, F = >=F0.  A cheap detector flags any
-// step that may contain a bad byte ("must be continuation" xor C, plus the
-// special second-byte / overlong / range checks); a flagged step is resolved
-// by the exact predicate above (u8_bad_at), which is the only place error
-// offsets come from.
+// Work layout: a warp owns a contiguous 2 KiB chunk of its CTA's 16 KiB tile
+// and walks it in 4 rounds of 512 B; in a round lane l holds bytes
+// [16l, 16l+16) in registers (one coalesced 16-byte load), i.e. four 32-bit
+// "quads".  Neighbour quads come from warp shuffles.  Per quad the kernels
+// build SWAR byte masks (bit 7 of each byte): C = continuation, L = >=C0,
+// E = >=E0, F = >=F0.  A cheap detector ("must be a continuation" xor C, the
+// C0/C1 test, and second-byte range tests behind a warp-uniform prefilter)
+// flags any round that may hold a bad byte; a flagged round is resolved by
+// the exact predicate (u8_bad_at), the only source of error offsets.
 #pragma once
 
 #include "lu_common.cuh"
@@ -39,36 +42,6 @@ __device__ __forceinline__ U8Masks u8_classify(uint32_t x)
     m.E = m.L & (x << 2);
     m.F = m.E & (x << 3);
     return m;
-}
-
-// bit 7 set in each byte that is zero
-__device__ __forceinline__ uint32_t zero8(uint32_t v)
-{
-    return ~(((v & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | v) & H8;
-}
-
-// Detector: nonzero if a bad byte may lie in this quad (or the first three
-// bytes of the following quad belong to a lead of this quad with a missing
-// continuation, which the next quad's "must ^ C" reports).  Never misses the
-// first bad byte of the input ("detector completeness").
-__device__ __forceinline__ uint32_t u8_detect(uint32_t x, uint32_t xn, const U8Masks &m, const U8Masks &p,
-                                              bool any_f)
-{
-    const uint32_t must = fsl(p.L, m.L, 8) | fsl(p.E, m.E, 16) | fsl(p.F, m.F, 24);
-    uint32_t d = must ^ m.C;
-    // C0 / C1: 2-byte leads whose payload bits 4..1 are zero
-    d |= m.L & ~m.E & ~((x & 0x1E1E1E1Eu) + 0x7F7F7F7Fu);
-    // E0 80..9F (overlong) / ED A0..BF (surrogate): hi byte of the decoded
-    // word & 0xF8 is 0x00 or 0xD8
-    const uint32_t n1 = fsr(x, xn, 8);
-    const uint32_t h = ((x << 4) & 0xF0F0F0F0u) | ((n1 >> 2) & 0x08080808u);
-    d |= m.E & ~m.F & (zero8(h) | zero8(h ^ 0xD8D8D8D8u));
-    if (any_f) {
-        // F0 80..8F (overlong), F4 90.. / F5..F7 (> U+10FFFF), F8..FF
-        const uint32_t key = ((x & 0x07070707u) << 2) | ((n1 >> 4) & 0x03030303u);
-        d |= m.F & (~(key + 0x7F7F7F7Fu) | (key + 0x6F6F6F6Fu) | (x << 4));
-    }
-    return d;
 }
 
 // Exact reference predicate for the byte at p (bytes p[-3..3] readable).
@@ -105,14 +78,51 @@ __device__ __forceinline__ bool u8_bad_at(const uint8_t *p)
     return false;
 }
 
-// first bad byte (0..3) of the quad at in_s[q], 4 if none
-__device__ __forceinline__ uint32_t u8_first_bad_quad(const uint32_t *in_s, int q)
+// byte at aligned-frame offset a, 0 outside [lo, hi) (rare paths only)
+__device__ __forceinline__ uint32_t gbyte(const uint8_t *base, int64_t a, int64_t lo, int64_t hi)
 {
-    const uint8_t *b = reinterpret_cast<const uint8_t *>(in_s + q);
-    for (uint32_t k = 0; k < 4; ++k)
-        if (u8_bad_at(b + k))
-            return k;
-    return 4;
+    return (a >= lo && a < hi) ? (uint32_t)base[a] : 0u;
+}
+
+__device__ __forceinline__ bool u8_bad_global(const uint8_t *base, int64_t a, int64_t lo, int64_t hi)
+{
+    uint8_t w[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k)
+        w[k] = (uint8_t)gbyte(base, a - 3 + k, lo, hi);
+    return u8_bad_at(w + 3);
+}
+
+// emit mask of the quad at aligned offset a (rare path: error fix-ups)
+__device__ __forceinline__ uint32_t u8_emit_global(const uint8_t *base, int64_t a, int64_t lo, int64_t hi)
+{
+    uint32_t x = 0, xp = 0, vm = 0;
+    for (int k = 0; k < 4; ++k) {
+        x |= gbyte(base, a + k, lo, hi) << (8 * k);
+        xp |= gbyte(base, a - 4 + k, lo, hi) << (8 * k);
+        if (a + k >= lo && a + k < hi)
+            vm |= 0x80u << (8 * k);
+    }
+    const U8Masks m = u8_classify(x), p = u8_classify(xp);
+    return (~m.C | fsl(p.F, m.F, 8)) & H8 & vm;
+}
+
+__device__ __forceinline__ uint4 ld16(const uint8_t *base, int64_t a, int64_t lo, int64_t hi, bool boundary)
+{
+    if (!boundary)
+        return __ldcs(reinterpret_cast<const uint4 *>(base + a));
+    if (a + 16 <= lo || a >= hi)
+        return make_uint4(0, 0, 0, 0);
+    return load_u128_masked(base, a, lo, hi);
+}
+
+__device__ __forceinline__ uint32_t ld4(const uint8_t *base, int64_t a, int64_t lo, int64_t hi)
+{
+    if (a + 4 <= lo || a >= hi)
+        return 0u;
+    if (a >= lo && a + 4 <= hi)
+        return __ldg(reinterpret_cast<const uint32_t *>(base + a));
+    return load_u32_masked(base, a, lo, hi);
 }
 
 struct WarpResult {
@@ -122,13 +132,57 @@ struct WarpResult {
     uint32_t pad;
 };
 
+// One round's detector + masks, shared by K1 and K3.
+struct U8Round {
+    uint32_t w[6]; // xp, q0..q3, xn
+    U8Masks m[5];  // masks of w[0..4]
+    uint32_t det;  // nonzero: a bad byte may lie in this lane's 16 bytes
+    uint32_t any4; // F lead or low-surrogate position present
+};
+
+__device__ __forceinline__ void u8_round_detect(U8Round &R)
+{
+    R.m[0] = u8_classify(R.w[0]);
+    uint32_t det = 0, pe = 0, anyf = 0;
+#pragma unroll
+    for (int k = 1; k <= 4; ++k) {
+        R.m[k] = u8_classify(R.w[k]);
+        const U8Masks &c = R.m[k], &p = R.m[k - 1];
+        const uint32_t x = R.w[k];
+        const uint32_t must = fsl(p.L, c.L, 8) | fsl(p.E, c.E, 16) | fsl(p.F, c.F, 24);
+        det |= must ^ c.C;
+        // C0 / C1: 2-byte leads with payload bits 4..1 clear
+        det |= c.L & ~c.E & ~((x & 0x1E1E1E1Eu) + 0x7F7F7F7Fu);
+        // prefilter for E0 / ED (and EE / EF): E-class with low nibble in {0, D, E, F}
+        const uint32_t v = x + 0x03030303u;
+        pe |= c.E & ~(v << 4) & ~(v << 5);
+        anyf |= c.F;
+    }
+    R.any4 = anyf;
+    if (__any_sync(0xffffffffu, (pe | anyf) != 0)) {
+#pragma unroll
+        for (int k = 1; k <= 4; ++k) {
+            const U8Masks &c = R.m[k];
+            const uint32_t x = R.w[k];
+            const uint32_t n1 = fsr(x, R.w[k + 1], 8);
+            // E0 80..9F (overlong), ED A0..BF (surrogate): u = (b&0xF)<<1 | bit5(c1) in {0, 27}
+            const uint32_t u = ((x & 0x0F0F0F0Fu) << 1) | ((n1 >> 5) & 0x01010101u);
+            det |= c.E & ~c.F & ~((u + 0x7F7F7F7Fu) & ((u ^ 0x1B1B1B1Bu) + 0x7F7F7F7Fu));
+            // F0 80..8F (overlong), F4 90.. / F5..F7 (> U+10FFFF), F8..FF
+            const uint32_t key = ((x & 0x07070707u) << 2) | ((n1 >> 4) & 0x03030303u);
+            det |= c.F & (~(key + 0x7F7F7F7Fu) | (key + 0x6F6F6F6Fu) | (x << 4));
+        }
+    }
+    R.det = det;
+}
+
 // ============================================================ K1: utf8->utf16
 
 struct alignas(8) SelPair {
     uint32_t s01, s23;
 };
 
-// words of a quad: lo/hi byte planes -> up to four packed UTF-16 words
+// lo/hi byte planes of the UTF-16 word emitted at each byte position
 __device__ __forceinline__ void u8_decode_quad(uint32_t x, uint32_t xn, const U8Masks &m, uint32_t fi1, bool any4,
                                                uint32_t &lo, uint32_t &hi)
 {
@@ -139,15 +193,13 @@ __device__ __forceinline__ void u8_decode_quad(uint32_t x, uint32_t xn, const U8
     const uint32_t lo2 = ((x << 6) & 0xC0C0C0C0u) | (n1 & 0x3F3F3F3Fu);
     const uint32_t hi2 = (x >> 2) & 0x07070707u;
     const uint32_t sA = sgn8(x);
-    const uint32_t sL = sgn8(m.L);
-    const uint32_t sE = sgn8(m.E);
-    const uint32_t sF = sgn8(m.F);
-    const uint32_t sS = sgn8(m.C & fi1); // first continuation after an F lead: low surrogate
-    const uint32_t s2 = sL & ~sE;
-    const uint32_t s3 = sE & ~sF;
-    lo = (x & ~sA) | (lo2 & s2) | (lo3 & (s3 | sS));
+    const uint32_t s2 = sgn8(m.L & ~m.E);
+    const uint32_t s3 = sgn8(m.E & ~m.F);
+    lo = (x & ~sA) | (lo2 & s2) | (lo3 & s3);
     hi = (hi2 & s2) | (hi3 & s3);
     if (any4) {
+        const uint32_t sF = sgn8(m.F);
+        const uint32_t sS = sgn8(m.C & fi1); // first continuation after an F lead: low surrogate
         // high surrogate at the lead: 0xD7C0 + (cp >> 10)
         const uint32_t mm = ((n1 << 2) & 0xFCFCFCFCu) | ((n2 >> 4) & 0x03030303u);
         const uint32_t lo4 = ((mm | H8) - 0x40404040u) ^ (~mm & H8); // bytewise mm - 0x40
@@ -155,66 +207,93 @@ __device__ __forceinline__ void u8_decode_quad(uint32_t x, uint32_t xn, const U8
         const uint32_t hi4 = (x & 0x07070707u) + carry + 0xD7D7D7D7u;
         // low surrogate at the first continuation: 0xDC00 | cp & 0x3FF
         const uint32_t hiS = 0xDCDCDCDCu | ((n1 >> 2) & 0x03030303u);
-        lo |= lo4 & sF;
+        lo |= (lo4 & sF) | (lo3 & sS);
         hi |= (hi4 & sF) | (hiS & sS);
     }
 }
 
+__device__ __forceinline__ void sts16(uint32_t addr, uint32_t v)
+{
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void sts16_if(uint32_t addr, uint32_t v, uint32_t room, uint32_t j)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.gt.u32 p, %2, %3;\n\t@p st.shared.u16 [%0], %1;\n\t}" ::"r"(addr),
+                 "h"((unsigned short)v), "r"(room), "r"(j)
+                 : "memory");
+}
+
 template <bool Boundary>
-__device__ __forceinline__ void u8u16_warp(const uint32_t *in_s, uint16_t *out_w, const SelPair *sel,
-                                           int64_t tile_off, int64_t lo_b, int64_t hi_b, WarpResult &wr)
+__device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
+                                           int64_t hi_b, uint16_t *out_w, const SelPair *sel, WarpResult &wr)
 {
     const uint32_t lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
-    const int q0 = kInHead + (int)warp * kChunkQuads;
-    uint32_t running = 0;
-    uint32_t err = 0, err_pos = 0, units = 0;
-
-#pragma unroll 1
-    for (int g = 0; g < kGroups; ++g) {
-        uint32_t x[kGroup], xn[kGroup], fi1[kGroup], e[kGroup];
-        U8Masks mk[kGroup];
-        uint32_t det = 0, pk = 0;
-        const int qg = q0 + g * kGroup * 32;
+    const int64_t chunk = tile_off + (int64_t)warp * kChunkBytes;
+    constexpr int kRounds = kChunkBytes / 512;
+    uint4 q[kRounds];
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) {
-            const int q = qg + j * 32 + (int)lane;
-            x[j] = in_s[q];
-            const uint32_t xp = in_s[q - 1];
-            xn[j] = in_s[q + 1];
-            mk[j] = u8_classify(x[j]);
-            const U8Masks mp = u8_classify(xp);
-            fi1[j] = fsl(mp.F, mk[j].F, 8);
-            e[j] = (~mk[j].C | fi1[j]) & H8;
-            if (Boundary)
-                e[j] &= valid_mask(tile_off + 4 * (int64_t)(q - kInHead), lo_b, hi_b);
-            const bool any_f = __any_sync(0xffffffffu, (mk[j].F | mp.F) != 0);
-            det |= u8_detect(x[j], xn[j], mk[j], mp, any_f);
-            pk |= (uint32_t)__popc(e[j]) << (8 * j);
-        }
-        if (g == kGroups - 1 && lane == 31) {
+    for (int r = 0; r < kRounds; ++r)
+        q[r] = ld16(base, chunk + r * 512 + 16 * (int64_t)lane, lo_b, hi_b, Boundary);
+    uint32_t carry = (lane == 0) ? ld4(base, chunk - 4, lo_b, hi_b) : 0u;
+    const uint32_t halo_n = (lane == 31) ? ld4(base, chunk + kChunkBytes, lo_b, hi_b) : 0u;
+    uint32_t rn[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r)
+        rn[r] = __shfl_sync(0xffffffffu, q[r].x, (lane + 1) & 31);
+
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(out_w);
+    uint32_t running = 0, err = 0, err_pos = 0, units = 0;
+
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t lane_off = chunk + r * 512 + 16 * (int64_t)lane;
+        const uint32_t rp = __shfl_sync(0xffffffffu, q[r].w, (lane + 31) & 31);
+        U8Round R;
+        R.w[0] = (lane == 0) ? carry : rp;
+        carry = rp;
+        R.w[1] = q[r].x;
+        R.w[2] = q[r].y;
+        R.w[3] = q[r].z;
+        R.w[4] = q[r].w;
+        R.w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : halo_n) : rn[r];
+        u8_round_detect(R);
+        if (r == kRounds - 1 && lane == 31) {
             // chunk end: leads of the last quad whose continuations lie past the chunk
-            const uint32_t cn = u8_classify(xn[kGroup - 1]).C;
-            const U8Masks &m = mk[kGroup - 1];
-            const uint32_t c = m.C;
-            det |= (m.L & ~fsr(c, cn, 8)) | (m.E & ~fsr(c, cn, 16)) | (m.F & ~fsr(c, cn, 24));
+            const uint32_t cn = u8_classify(R.w[5]).C;
+            const U8Masks &m = R.m[4];
+            R.det |= (m.L & ~fsr(m.C, cn, 8)) | (m.E & ~fsr(m.C, cn, 16)) | (m.F & ~fsr(m.C, cn, 24));
         }
-        const uint32_t incl = warp_scan_packed(pk);
-        const uint32_t excl = incl - pk;
+        uint32_t e[4], fi1[4], c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            fi1[k] = fsl(R.m[k].F, R.m[k + 1].F, 8);
+            e[k] = (~R.m[k + 1].C | fi1[k]) & H8;
+            if (Boundary)
+                e[k] &= valid_mask(lane_off + 4 * k, lo_b, hi_b);
+            c[k] = (uint32_t)__popc(e[k]);
+        }
+        const uint32_t cnt = c[0] + c[1] + c[2] + c[3];
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= (uint32_t)d)
+                incl += o;
+        }
+        const uint32_t excl = incl - cnt;
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
 
-        if (__any_sync(0xffffffffu, det != 0)) {
-            // exact resolution, in stream order
+        if (__any_sync(0xffffffffu, R.det != 0)) {
+            // exact resolution in stream order: tail of the previous round first
+            const int64_t rstart = chunk + r * 512;
             bool found = false;
-            if (g > 0) {
-                // the three bytes before the group (a lead there may miss a
-                // continuation that only this group's detector saw)
+            if (r > 0) {
                 uint32_t tb = 3;
                 if (lane == 0) {
-                    const uint8_t *b = reinterpret_cast<const uint8_t *>(in_s + qg);
-                    for (uint32_t k = 0; k < 3; ++k)
-                        if (u8_bad_at(b - 3 + (int)k)) {
-                            tb = k;
+                    for (uint32_t t = 0; t < 3; ++t)
+                        if (u8_bad_global(base, rstart - 3 + t, lo_b, hi_b)) {
+                            tb = t;
                             break;
                         }
                 }
@@ -222,70 +301,86 @@ __device__ __forceinline__ void u8u16_warp(const uint32_t *in_s, uint16_t *out_w
                 if (tb < 3) {
                     uint32_t drop = 0;
                     if (lane == 0) {
-                        const uint32_t xq = in_s[qg - 1];
-                        const U8Masks mq = u8_classify(xq);
-                        const U8Masks mqq = u8_classify(in_s[qg - 2]);
-                        uint32_t eq = (~mq.C | fsl(mqq.F, mq.F, 8)) & H8;
-                        if (Boundary)
-                            eq &= valid_mask(tile_off + 4 * (int64_t)(qg - 1 - kInHead), lo_b, hi_b);
-                        // bytes 1+tb .. 3 of that quad are at or after the error
-                        eq &= ~((1u << (8 * (1 + tb))) - 1u);
-                        drop = (uint32_t)__popc(eq);
+                        // emits of the previous round's last quad at or after the error
+                        const uint32_t eq = u8_emit_global(base, rstart - 4, lo_b, hi_b);
+                        drop = (uint32_t)__popc(eq & ~((1u << (8 * (1 + tb))) - 1u));
                     }
                     drop = __shfl_sync(0xffffffffu, drop, 0);
                     err = 1;
-                    err_pos = 4u * (uint32_t)(qg - kInHead) - 3u + tb;
+                    err_pos = (uint32_t)(rstart - 3 + tb - tile_off);
                     units = running - drop;
                     found = true;
                 }
             }
-            uint32_t before = running;
-#pragma unroll
-            for (int j = 0; j < kGroup; ++j) {
-                if (!found) {
-                    const int q = qg + j * 32 + (int)lane;
-                    const uint32_t kb = u8_first_bad_quad(in_s, q);
-                    const uint32_t bm = __ballot_sync(0xffffffffu, kb < 4);
-                    if (bm) {
-                        const uint32_t fl = (uint32_t)__ffs(bm) - 1;
-                        const uint32_t within = (uint32_t)__popc(e[j] & ((1u << (8 * (kb & 3))) - 1u)) +
-                                                ((excl >> (8 * j)) & 0xFFu);
-                        const uint32_t kbf = __shfl_sync(0xffffffffu, kb, fl);
-                        const uint32_t wf = __shfl_sync(0xffffffffu, within, fl);
-                        err = 1;
-                        err_pos = 4u * (uint32_t)(qg + j * 32 + (int)fl - kInHead) + kbf;
-                        units = before + wf;
-                        found = true;
-                    }
+            if (!found) {
+                // a lead missing a continuation is flagged at the continuation
+                // slot, possibly in the next lane: scan when either lane flagged
+                const uint32_t scan = R.det | __shfl_down_sync(0xffffffffu, R.det, 1);
+                uint32_t kb = 16;
+                if (scan != 0) {
+                    for (uint32_t t = 0; t < 16; ++t)
+                        if (u8_bad_global(base, lane_off + t, lo_b, hi_b)) {
+                            kb = t;
+                            break;
+                        }
                 }
-                before += (tot >> (8 * j)) & 0xFFu;
+                const uint32_t bm = __ballot_sync(0xffffffffu, kb < 16);
+                if (bm) {
+                    const uint32_t fl = (uint32_t)__ffs(bm) - 1;
+                    uint32_t em = 0;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        em |= ((e[k] * 0x00204081u) >> 28) << (4 * k);
+                    const uint32_t within = excl + (uint32_t)__popc(em & ((1u << (kb & 15)) - 1u));
+                    const uint32_t kbf = __shfl_sync(0xffffffffu, kb, fl);
+                    const uint32_t wf = __shfl_sync(0xffffffffu, within, fl);
+                    err = 1;
+                    err_pos = (uint32_t)(rstart - tile_off) + 16 * fl + kbf;
+                    units = running + wf;
+                }
             }
         }
 
         // decode + compact into the warp's staging region
-        uint32_t base = running;
+        const bool any4 = __any_sync(0xffffffffu, (R.any4 | R.m[0].F) != 0);
+        uint32_t off = running + excl;
+        const uint32_t lane_end = off + cnt;
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) {
-            const bool any4 = __any_sync(0xffffffffu, (mk[j].F | (mk[j].C & fi1[j])) != 0);
+        for (int k = 0; k < 4; ++k) {
             uint32_t lo, hi;
-            u8_decode_quad(x[j], xn[j], mk[j], fi1[j], any4, lo, hi);
-            const uint32_t idx = (e[j] * 0x00204081u) >> 28;
+            u8_decode_quad(R.w[k + 1], R.w[k + 2], R.m[k + 1], fi1[k], any4, lo, hi);
+            const uint32_t idx = (e[k] * 0x00204081u) >> 28;
             const SelPair sp = sel[idx];
             const uint32_t w01 = prmt(lo, hi, sp.s01);
             const uint32_t w23 = prmt(lo, hi, sp.s23);
-            const uint32_t c = (uint32_t)__popc(e[j]);
-            uint16_t *dst = out_w + base + ((excl >> (8 * j)) & 0xFFu);
-            if (c > 0)
-                dst[0] = (uint16_t)w01;
-            if (c > 1)
-                dst[1] = (uint16_t)(w01 >> 16);
-            if (c > 2)
-                dst[2] = (uint16_t)w23;
-            if (c > 3)
-                dst[3] = (uint16_t)(w23 >> 16);
-            base += (tot >> (8 * j)) & 0xFFu;
+            const uint32_t a = sbase + 2 * off;
+            const uint32_t room = lane_end - off;
+            // Stores past this quad's words are overwritten by the next
+            // quad's stores (program order); only slots that valid input
+            // could push into the next lane's region are predicated.
+            if (Boundary) {
+                sts16_if(a, w01, room, 0);
+                sts16_if(a + 2, w01 >> 16, room, 1);
+                sts16_if(a + 4, w23, room, 2);
+                sts16_if(a + 6, w23 >> 16, room, 3);
+            } else {
+                sts16(a, w01);
+                if (k < 3)
+                    sts16(a + 2, w01 >> 16);
+                else
+                    sts16_if(a + 2, w01 >> 16, room, 1);
+                if (k < 2)
+                    sts16(a + 4, w23);
+                else
+                    sts16_if(a + 4, w23, room, 2);
+                if (k < 1)
+                    sts16(a + 6, w23 >> 16);
+                else
+                    sts16_if(a + 6, w23 >> 16, room, 3);
+            }
+            off += c[k];
         }
-        running = base;
+        running += tot;
         if (err)
             break;
     }
@@ -301,53 +396,72 @@ __device__ __forceinline__ void u8u16_warp(const uint32_t *in_s, uint16_t *out_w
 // ============================================================ K3: validate
 
 template <bool Boundary>
-__device__ __forceinline__ void u8val_warp(const uint32_t *in_s, int64_t tile_off, int64_t lo_b, int64_t hi_b,
-                                           WarpResult &wr)
+__device__ __forceinline__ void u8val_warp(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
+                                           int64_t hi_b, WarpResult &wr)
 {
-    (void)tile_off;
-    (void)lo_b;
-    (void)hi_b;
     const uint32_t lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
-    const int q0 = kInHead + (int)warp * kChunkQuads;
+    const int64_t chunk = tile_off + (int64_t)warp * kChunkBytes;
+    constexpr int kRounds = kChunkBytes / 512;
+    uint4 q[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r)
+        q[r] = ld16(base, chunk + r * 512 + 16 * (int64_t)lane, lo_b, hi_b, Boundary);
+    uint32_t carry = (lane == 0) ? ld4(base, chunk - 4, lo_b, hi_b) : 0u;
+    const uint32_t halo_n = (lane == 31) ? ld4(base, chunk + kChunkBytes, lo_b, hi_b) : 0u;
+    uint32_t rn[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r)
+        rn[r] = __shfl_sync(0xffffffffu, q[r].x, (lane + 1) & 31);
     uint32_t err = 0, err_pos = 0;
-#pragma unroll 4
-    for (int s = 0; s < kSteps; ++s) {
-        const int q = q0 + s * 32 + (int)lane;
-        const uint32_t x = in_s[q];
-        const uint32_t xp = in_s[q - 1];
-        const uint32_t xn = in_s[q + 1];
-        const U8Masks m = u8_classify(x);
-        const U8Masks mp = u8_classify(xp);
-        const bool any_f = __any_sync(0xffffffffu, (m.F | mp.F) != 0);
-        uint32_t det = u8_detect(x, xn, m, mp, any_f);
-        if (s == kSteps - 1 && lane == 31) {
-            const uint32_t cn = u8_classify(xn).C;
-            det |= (m.L & ~fsr(m.C, cn, 8)) | (m.E & ~fsr(m.C, cn, 16)) | (m.F & ~fsr(m.C, cn, 24));
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const uint32_t rp = __shfl_sync(0xffffffffu, q[r].w, (lane + 31) & 31);
+        U8Round R;
+        R.w[0] = (lane == 0) ? carry : rp;
+        carry = rp;
+        R.w[1] = q[r].x;
+        R.w[2] = q[r].y;
+        R.w[3] = q[r].z;
+        R.w[4] = q[r].w;
+        R.w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : halo_n) : rn[r];
+        u8_round_detect(R);
+        if (r == kRounds - 1 && lane == 31) {
+            const uint32_t cn = u8_classify(R.w[5]).C;
+            const U8Masks &m = R.m[4];
+            R.det |= (m.L & ~fsr(m.C, cn, 8)) | (m.E & ~fsr(m.C, cn, 16)) | (m.F & ~fsr(m.C, cn, 24));
         }
-        if (__any_sync(0xffffffffu, det != 0)) {
-            const int qs = q0 + s * 32;
+        if (__any_sync(0xffffffffu, R.det != 0)) {
+            const int64_t rstart = chunk + r * 512;
             uint32_t tb = 3;
-            if (s > 0 && lane == 0) {
-                const uint8_t *b = reinterpret_cast<const uint8_t *>(in_s + qs);
-                for (uint32_t k = 0; k < 3; ++k)
-                    if (u8_bad_at(b - 3 + (int)k)) {
-                        tb = k;
+            if (r > 0 && lane == 0) {
+                for (uint32_t t = 0; t < 3; ++t)
+                    if (u8_bad_global(base, rstart - 3 + t, lo_b, hi_b)) {
+                        tb = t;
                         break;
                     }
             }
             tb = __shfl_sync(0xffffffffu, tb, 0);
             if (tb < 3) {
                 err = 1;
-                err_pos = 4u * (uint32_t)(qs - kInHead) - 3u + tb;
+                err_pos = (uint32_t)(rstart - 3 + tb - tile_off);
                 break;
             }
-            const uint32_t kb = u8_first_bad_quad(in_s, q);
-            const uint32_t bm = __ballot_sync(0xffffffffu, kb < 4);
+            uint32_t kb = 16;
+            const uint32_t scan = R.det | __shfl_down_sync(0xffffffffu, R.det, 1);
+            if (scan != 0) {
+                const int64_t lane_off = rstart + 16 * (int64_t)lane;
+                for (uint32_t t = 0; t < 16; ++t)
+                    if (u8_bad_global(base, lane_off + t, lo_b, hi_b)) {
+                        kb = t;
+                        break;
+                    }
+            }
+            const uint32_t bm = __ballot_sync(0xffffffffu, kb < 16);
             if (bm) {
                 const uint32_t fl = (uint32_t)__ffs(bm) - 1;
                 err = 1;
-                err_pos = 4u * (uint32_t)(qs + (int)fl - kInHead) + __shfl_sync(0xffffffffu, kb, fl);
+                err_pos = (uint32_t)(rstart - tile_off) + 16 * fl + __shfl_sync(0xffffffffu, kb, fl);
                 break;
             }
         }
