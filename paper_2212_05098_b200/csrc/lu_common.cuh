@@ -173,6 +173,66 @@ __device__ __forceinline__ uint64_t lookback(uint64_t *status, uint32_t tile, ui
     return excl;
 }
 
+// Central scanner, run by one warp for the whole grid.  Tiles publish only
+// their aggregate (flag 1); the scanner sweeps the status array in tile order,
+// 32*K entries per pass, and replaces each ready entry by flag 2 | EXCLUSIVE
+// prefix.  One pass covers up to 32*K tiles per L2 round trip, and no tile
+// ever waits on an inclusive-prefix chain: a tile's owner just polls its own
+// status word.  It stops at the first tile whose aggregate is not yet
+// published, so every claimed tile must publish without waiting on anything.
+template <int K>
+__device__ __forceinline__ void scan_tiles(uint64_t *status, uint32_t ntiles)
+{
+    const uint32_t lane = lane_id();
+    uint32_t next = 0;
+    uint64_t acc = 0;
+    while (next < ntiles) {
+        uint64_t s[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const uint32_t t = next + lane * K + j;
+            s[j] = t < ntiles ? ld_acquire(&status[t]) : 0ull;
+        }
+        uint32_t r = K; // leading ready entries of this lane's slice
+#pragma unroll
+        for (int j = K - 1; j >= 0; --j)
+            if ((s[j] >> kFlagShift) == 0)
+                r = j;
+        const uint32_t full = __ballot_sync(0xffffffffu, r == K);
+        const uint32_t f = full == 0xffffffffu ? 32u : (uint32_t)__ffs(~full) - 1;
+        const uint32_t myr = lane < f ? K : (lane == f ? r : 0u);
+        const uint32_t total = __reduce_add_sync(0xffffffffu, myr);
+        if (total == 0) {
+            __nanosleep(64);
+            continue;
+        }
+        uint64_t sum = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if ((uint32_t)j < myr)
+                sum = seq_combine(sum, s[j] & (kErrBit | kValMask));
+        uint64_t inc = sum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint64_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= (uint32_t)d)
+                inc = seq_combine(o, inc);
+        }
+        uint64_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
+        if (lane == 0)
+            ex = 0;
+        uint64_t run = seq_combine(acc, ex);
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if ((uint32_t)j < myr) {
+                st_release(&status[next + lane * K + j], kFlagInc | run);
+                run = seq_combine(run, s[j] & (kErrBit | kValMask));
+            }
+        acc = seq_combine(acc, __shfl_sync(0xffffffffu, inc, 31));
+        next += total;
+    }
+}
+
 // ------------------------------------------------------- tile staging loads
 
 // Loads the 16 KiB tile at aligned byte offset tile_off (relative to the

@@ -52,23 +52,45 @@ __device__ __forceinline__ void copy_out_u16(const uint16_t *src, uint32_t cnt, 
     uint16_t *dst = out_a + (g0 - shift); // 16-byte aligned
     const uint32_t total = shift + cnt;   // words from the aligned start
     const uint32_t full_lo = shift ? 1u : 0u, full_hi = total >> 3;
-    const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
-    if (shift == 0) {
-        const uint4 *s128 = reinterpret_cast<const uint4 *>(src);
-        for (uint32_t c = full_lo + lane; c < full_hi; c += 32)
-            __stcs(reinterpret_cast<uint4 *>(dst) + c, s128[c]);
-    } else if ((shift & 1) == 0) {
-        for (uint32_t c = full_lo + lane; c < full_hi; c += 32) {
-            const uint32_t m = (8 * c - shift) >> 1;
-            __stcs(reinterpret_cast<uint4 *>(dst) + c, make_uint4(s32[m], s32[m + 1], s32[m + 2], s32[m + 3]));
+    // Each output chunk straddles two aligned 16-byte staging vectors; read
+    // both with conflict-free LDS.128 and select the window (warp-uniform
+    // word offset r) in registers.
+    const uint4 *s128 = reinterpret_cast<const uint4 *>(src);
+    const uint32_t r = (8u - shift) & 7u;
+    for (uint32_t c = full_lo + lane; c < full_hi; c += 32) {
+        const uint32_t v = (8 * c - shift) >> 3;
+        const uint4 a = s128[v];
+        uint4 o;
+        if (r == 0) {
+            o = a;
+        } else {
+            const uint4 b = s128[v + 1];
+            const uint32_t w0 = a.x, w1 = a.y, w2 = a.z, w3 = a.w, w4 = b.x, w5 = b.y, w6 = b.z, w7 = b.w;
+            switch (r) {
+            case 1:
+                o = make_uint4(prmt(w0, w1, 0x5432), prmt(w1, w2, 0x5432), prmt(w2, w3, 0x5432), prmt(w3, w4, 0x5432));
+                break;
+            case 2:
+                o = make_uint4(w1, w2, w3, w4);
+                break;
+            case 3:
+                o = make_uint4(prmt(w1, w2, 0x5432), prmt(w2, w3, 0x5432), prmt(w3, w4, 0x5432), prmt(w4, w5, 0x5432));
+                break;
+            case 4:
+                o = make_uint4(w2, w3, w4, w5);
+                break;
+            case 5:
+                o = make_uint4(prmt(w2, w3, 0x5432), prmt(w3, w4, 0x5432), prmt(w4, w5, 0x5432), prmt(w5, w6, 0x5432));
+                break;
+            case 6:
+                o = make_uint4(w3, w4, w5, w6);
+                break;
+            default:
+                o = make_uint4(prmt(w3, w4, 0x5432), prmt(w4, w5, 0x5432), prmt(w5, w6, 0x5432), prmt(w6, w7, 0x5432));
+                break;
+            }
         }
-    } else {
-        for (uint32_t c = full_lo + lane; c < full_hi; c += 32) {
-            const uint32_t m = (8 * c - shift - 1) >> 1;
-            const uint32_t w0 = s32[m], w1 = s32[m + 1], w2 = s32[m + 2], w3 = s32[m + 3], w4 = s32[m + 4];
-            __stcs(reinterpret_cast<uint4 *>(dst) + c, make_uint4(prmt(w0, w1, 0x5432), prmt(w1, w2, 0x5432),
-                                                                  prmt(w2, w3, 0x5432), prmt(w3, w4, 0x5432)));
-        }
+        __stcs(reinterpret_cast<uint4 *>(dst) + c, o);
     }
     // partial chunks: head (chunk 0 when shift > 0) and tail (chunk full_hi)
     if (lane < 16) {
@@ -170,18 +192,18 @@ __device__ __forceinline__ void sel_table_init(SelPair *sel)
 
 // ====================================================== pipelined transcode
 //
-// Persistent CTAs (grid = resident capacity), each walking tiles
-// blockIdx.x, blockIdx.x + gridDim.x, ...  Warps 0..7 compute a tile into one
-// of two staging buffers; warp 8 is the look-back warp: it combines the warp
-// results, publishes the tile aggregate, resolves the exclusive prefix and
-// hands it back through a named barrier.  Meanwhile the compute warps already
-// work on the next tile, and only copy a tile out once its prefix is known,
-// so look-back latency overlaps compute instead of idling the CTA.
+// Persistent CTAs (grid = resident capacity).  Warps 0..7 claim tiles from a
+// ticket counter just before computing them (so tiles finish roughly in
+// ticket order), compute each into one of two shared staging buffers and
+// publish the tile aggregate.  One extra warp in CTA 0 runs the central
+// scanner (scan_tiles) that turns aggregates into exclusive prefixes.  A
+// buffer is copied out when it is about to be reused, two tiles later, by
+// which time its prefix is normally known, so prefix latency hides behind
+// compute.  Every CTA is resident and a tile publishes its aggregate before
+// waiting on anything, so progress is guaranteed.
 //
-// Named barriers: 1+b "tile in buffer b computed" (compute warps arrive, the
-// look-back warp syncs); 3+b "prefix of buffer b known" (look-back warp
-// arrives, compute warps sync).  Every CTA is resident, and a tile only waits
-// on smaller tile indices, so progress is guaranteed.
+// Named barriers (compute warps only, kThreads threads): 5 = ticket
+// broadcast, 6 = tile computed, 7 = prefix broadcast.
 
 constexpr int kPipeThreads = kThreads + 32;
 
@@ -190,51 +212,58 @@ struct PipeShared {
     uint32_t warp_excl[2][kWarps];
     uint64_t excl[2];
     uint32_t first_err[2];
-    uint32_t ticket[2];  // tile claimed for iteration i lives in ticket[i & 1]
-    uint32_t tile_of[2]; // tile held by each staging buffer (0xffffffff: stop)
+    uint32_t tile_of[2];
+    uint32_t claim;
 };
 
 __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n)
 {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-__device__ __forceinline__ void bar_arrive(uint32_t id, uint32_t n)
-{
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
-// Look-back warp body for one tile; unit_shift = 0 for byte positions (UTF-8
-// input), 1 for word positions (UTF-16 input).
-__device__ __forceinline__ void pipe_lookback(PipeShared &ps, uint32_t buf, uint32_t tile, uint64_t *status,
-                                              Outcome *res, uint32_t ntiles, int64_t lo_b, uint64_t n_units,
-                                              int unit_shift)
-{
-    const uint32_t lane = lane_id();
-    uint32_t first = kWarps, units = 0;
-    if (lane == 0) {
-        for (int w = 0; w < kWarps; ++w) {
-            ps.warp_excl[buf][w] = units;
-            units += ps.wres[buf][w].units;
-            if (ps.wres[buf][w].err) {
-                first = (uint32_t)w;
-                break;
-            }
-        }
-        ps.first_err[buf] = first;
+// Direction traits: UTF-8 -> UTF-16 (K1) and UTF-16 -> UTF-8 (K2).
+struct DirU8U16 {
+    using OutT = uint16_t;
+    static constexpr int kStride = kOutStrideU16;
+    static constexpr int kUnitShift = 0; // input positions are bytes
+    template <bool B>
+    __device__ static void compute(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, OutT *out_w,
+                                   const SelPair *sel, WarpResult &wr)
+    {
+        u8u16_warp<B>(base, tile_off, lo_b, hi_b, out_w, sel, wr);
     }
-    first = __shfl_sync(0xffffffffu, first, 0);
-    units = __shfl_sync(0xffffffffu, units, 0);
-    const uint64_t agg = (first < kWarps ? kErrBit : 0ull) | (uint64_t)units;
-    const uint64_t ex = lookback(status, tile, agg);
-    if (lane == 0) {
-        ps.excl[buf] = ex;
+    __device__ static void copy_out(const OutT *src, uint32_t cnt, OutT *out_a, uint64_t g0)
+    {
+        copy_out_u16(src, cnt, out_a, g0);
+    }
+};
+
+template <class Dir>
+__device__ __forceinline__ void pipe_copy_buffer(PipeShared &ps, uint32_t b, typename Dir::OutT *out_s,
+                                                 typename Dir::OutT *out_a, uint64_t out_lead, uint64_t *status,
+                                                 Outcome *res, uint32_t ntiles, int64_t lo_b, uint64_t n_units)
+{
+    const uint32_t warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        const uint32_t tile = ps.tile_of[b];
+        uint64_t st = ld_acquire(&status[tile]);
+        while ((st >> kFlagShift) != 2) {
+            __nanosleep(32);
+            st = ld_acquire(&status[tile]);
+        }
+        const uint64_t ex = st & (kErrBit | kValMask);
+        ps.excl[b] = ex;
         if (!(ex & kErrBit)) {
-            const uint64_t written = (ex & kValMask) + units;
+            const uint32_t first = ps.first_err[b];
+            uint64_t units = 0;
+            for (uint32_t w = 0; w < kWarps && w <= first; ++w)
+                units += ps.wres[b][w].units;
+            const uint64_t written = ex + units;
             const int64_t tile_off = (int64_t)tile * kTileBytes;
             if (first < kWarps) {
                 res->status = kStatusMalformed;
                 res->pad = 0;
-                res->consumed = (uint64_t)((tile_off + ps.wres[buf][first].pos - lo_b) >> unit_shift);
+                res->consumed = (uint64_t)((tile_off + ps.wres[b][first].pos - lo_b) >> Dir::kUnitShift);
                 res->written = written;
             } else if (tile == ntiles - 1) {
                 res->status = kStatusOk;
@@ -244,85 +273,73 @@ __device__ __forceinline__ void pipe_lookback(PipeShared &ps, uint32_t buf, uint
             }
         }
     }
+    bar_sync(7, kThreads);
+    const uint64_t ex = ps.excl[b];
+    if (!(ex & kErrBit) && warp <= ps.first_err[b])
+        Dir::copy_out(out_s + (b * kWarps + warp) * Dir::kStride, ps.wres[b][warp].units, out_a,
+                      ex + ps.warp_excl[b][warp] + out_lead);
 }
 
-// ===================================================================== K1
-
+template <class Dir>
 __global__ void __launch_bounds__(kPipeThreads, 3)
-    k_utf8_to_utf16le(const uint8_t *__restrict__ base, uint32_t lead, uint64_t n, uint16_t *__restrict__ out_a,
-                      uint32_t out_lead_words, uint64_t *__restrict__ status, Outcome *__restrict__ res,
-                      uint32_t ntiles)
+    k_transcode(const uint8_t *__restrict__ base, uint32_t lead, uint64_t n_units, uint64_t n_bytes,
+                typename Dir::OutT *__restrict__ out_a, uint32_t out_lead, uint64_t *__restrict__ status,
+                Outcome *__restrict__ res, uint32_t ntiles)
 {
+    using OutT = typename Dir::OutT;
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    uint16_t *out_s = reinterpret_cast<uint16_t *>(smem_raw); // [2][kWarps][kOutStrideU16]
+    OutT *out_s = reinterpret_cast<OutT *>(smem_raw); // [2][kWarps][stride]
     __shared__ SelPair sel[16];
     __shared__ PipeShared ps;
 
-    const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n;
+    const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n_bytes;
     unsigned int *ticket = reinterpret_cast<unsigned int *>(status + ntiles);
     sel_table_init(sel);
-    if (threadIdx.x == 0)
-        ps.ticket[0] = atomicAdd(ticket, 1u);
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5;
-
     if (warp == kWarps) {
-        for (uint32_t i = 0;; ++i) {
-            const uint32_t buf = i & 1;
-            bar_sync(1 + buf, kPipeThreads);
-            const uint32_t tile = ps.tile_of[buf];
-            if (tile >= ntiles)
-                break; // sentinel: the compute warps ran out of tiles
-            pipe_lookback(ps, buf, tile, status, res, ntiles, lo_b, n, 0);
-            bar_arrive(3 + buf, kPipeThreads);
-        }
+        if (blockIdx.x == 0)
+            scan_tiles<16>(status, ntiles);
         return;
     }
 
-    // Tiles are claimed just before they are computed (ticket order ==
-    // compute order), so a tile's look-back only waits on tiles that started
-    // earlier.
     uint32_t i = 0;
     for (;; ++i) {
         const uint32_t buf = i & 1;
-        const uint32_t tile = ps.ticket[buf];
-        if (tile >= ntiles) {
-            if (threadIdx.x == 0)
-                ps.tile_of[buf] = 0xffffffffu;
-            bar_arrive(1 + buf, kPipeThreads);
+        if (i >= 2) // buffer reuse: copy out the tile computed two iterations ago
+            pipe_copy_buffer<Dir>(ps, buf, out_s, out_a, out_lead, status, res, ntiles, lo_b, n_units);
+        if (threadIdx.x == 0)
+            ps.claim = atomicAdd(ticket, 1u);
+        bar_sync(5, kThreads);
+        const uint32_t tile = ps.claim;
+        if (tile >= ntiles)
             break;
-        }
         const int64_t tile_off = (int64_t)tile * kTileBytes;
-        uint16_t *out_w = out_s + (buf * kWarps + warp) * kOutStrideU16;
+        OutT *out_w = out_s + (buf * kWarps + warp) * Dir::kStride;
         const bool interior = (tile_off - 4 >= lo_b) && (tile_off + kTileBytes + 4 <= hi_b);
         if (interior)
-            u8u16_warp<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][warp]);
+            Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][warp]);
         else
-            u8u16_warp<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][warp]);
-        if (threadIdx.x == 0)
+            Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][warp]);
+        bar_sync(6, kThreads);
+        if (threadIdx.x == 0) {
+            uint32_t units = 0, first = kWarps;
+            for (int w = 0; w < kWarps; ++w) {
+                ps.warp_excl[buf][w] = units;
+                units += ps.wres[buf][w].units;
+                if (ps.wres[buf][w].err) {
+                    first = (uint32_t)w;
+                    break;
+                }
+            }
+            ps.first_err[buf] = first;
             ps.tile_of[buf] = tile;
-        bar_arrive(1 + buf, kPipeThreads);
-        if (threadIdx.x == 0)
-            ps.ticket[buf ^ 1] = atomicAdd(ticket, 1u); // next tile, claimed now
-        if (i == 0)
-            bar_sync(5, kThreads); // publish ps.ticket[1] to the compute warps
-        if (i > 0) {
-            const uint32_t pb = buf ^ 1;
-            bar_sync(3 + pb, kPipeThreads);
-            const uint64_t ex = ps.excl[pb];
-            if (!(ex & kErrBit) && warp <= ps.first_err[pb])
-                copy_out_u16(out_s + (pb * kWarps + warp) * kOutStrideU16, ps.wres[pb][warp].units, out_a,
-                             (ex & kValMask) + ps.warp_excl[pb][warp] + out_lead_words);
+            st_release(&status[tile], kFlagAgg | (first < kWarps ? kErrBit : 0ull) | (uint64_t)units);
         }
     }
-    if (i > 0) {
-        const uint32_t pb = (i - 1) & 1;
-        bar_sync(3 + pb, kPipeThreads);
-        const uint64_t ex = ps.excl[pb];
-        if (!(ex & kErrBit) && warp <= ps.first_err[pb])
-            copy_out_u16(out_s + (pb * kWarps + warp) * kOutStrideU16, ps.wres[pb][warp].units, out_a,
-                         (ex & kValMask) + ps.warp_excl[pb][warp] + out_lead_words);
-    }
+    // drain: the last one or two tiles (in iteration order)
+    if (i >= 1)
+        pipe_copy_buffer<Dir>(ps, (i - 1) & 1, out_s, out_a, out_lead, status, res, ntiles, lo_b, n_units);
 }
 
 // ===================================================================== K2
@@ -468,7 +485,7 @@ static int set_smem_attrs()
     static cudaError_t status = cudaSuccess;
     std::call_once(once, [] {
         cudaError_t e;
-        e = cudaFuncSetAttribute(k_utf8_to_utf16le, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemK1);
+        e = cudaFuncSetAttribute(k_transcode<DirU8U16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemK1);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(k_utf16le_to_utf8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemK2);
         if (e == cudaSuccess)
@@ -565,10 +582,10 @@ int lu_utf8_to_utf16le(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint6
     const uint32_t out_lead = (uint32_t)(((uintptr_t)out_safe & 15) >> 1);
     uint16_t *out_a = out_safe - out_lead;
     unsigned grid = 0;
-    rc = persistent_grid((const void *)k_utf8_to_utf16le, kPipeThreads, kSmemK1, nt, &grid);
+    rc = persistent_grid((const void *)k_transcode<DirU8U16>, kPipeThreads, kSmemK1, nt, &grid);
     if (rc)
         return rc;
-    k_utf8_to_utf16le<<<grid, kPipeThreads, kSmemK1, stream>>>(base, lead, n_bytes, out_a, out_lead,
+    k_transcode<DirU8U16><<<grid, kPipeThreads, kSmemK1, stream>>>(base, lead, n_bytes, n_bytes, out_a, out_lead,
                                                                    reinterpret_cast<uint64_t *>(ws),
                                                                    reinterpret_cast<Outcome *>(res), (uint32_t)nt);
     e = cudaGetLastError();

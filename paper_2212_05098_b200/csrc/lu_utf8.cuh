@@ -133,44 +133,106 @@ struct WarpResult {
 };
 
 // One round's detector + masks, shared by K1 and K3.
+//
+// Like the paper's engines (ASCII and 1/2-byte fast paths,
+// /root/reference/pkg/src/laneutf/utf8_to_utf16.py:245-276), a warp round
+// picks the cheapest exact path its bytes allow (warp-uniform votes):
+//   path 0  no byte >= E0 in the round or its look-behind: ASCII + 2-byte
+//           leads only, "must be continuation" = L(i-1);
+//   path 1  no F-class byte and no 2-byte lead: ASCII + 3-byte leads;
+//   path 2  everything else (general detector and decoder).
+// Every path flags every bad byte its class mix can contain.
 struct U8Round {
     uint32_t w[6]; // xp, q0..q3, xn
-    U8Masks m[5];  // masks of w[0..4]
+    U8Masks m[5];  // masks of w[0..4] (F only computed off path 0)
     uint32_t det;  // nonzero: a bad byte may lie in this lane's 16 bytes
-    uint32_t any4; // F lead or low-surrogate position present
+    int path;
 };
+
+// E0 80..9F (overlong) / ED A0..BF (surrogate): u = (b&0xF)<<1 | bit5(c1) in {0, 27}
+__device__ __forceinline__ uint32_t u8_check_e(uint32_t x, uint32_t n1, const U8Masks &c)
+{
+    const uint32_t u = ((x & 0x0F0F0F0Fu) << 1) | ((n1 >> 5) & 0x01010101u);
+    return c.E & ~c.F & ~((u + 0x7F7F7F7Fu) & ((u ^ 0x1B1B1B1Bu) + 0x7F7F7F7Fu));
+}
+// F0 80..8F (overlong), F4 90.. / F5..F7 (> U+10FFFF), F8..FF
+__device__ __forceinline__ uint32_t u8_check_f(uint32_t x, uint32_t n1, const U8Masks &c)
+{
+    const uint32_t key = ((x & 0x07070707u) << 2) | ((n1 >> 4) & 0x03030303u);
+    return c.F & (~(key + 0x7F7F7F7Fu) | (key + 0x6F6F6F6Fu) | (x << 4));
+}
+// E-class bytes whose low nibble is 0, D, E or F (E0 / ED candidates)
+__device__ __forceinline__ uint32_t u8_prefilter_e(uint32_t x, const U8Masks &c)
+{
+    const uint32_t v = x + 0x03030303u;
+    return c.E & ~(v << 4) & ~(v << 5);
+}
 
 __device__ __forceinline__ void u8_round_detect(U8Round &R)
 {
-    R.m[0] = u8_classify(R.w[0]);
-    uint32_t det = 0, pe = 0, anyf = 0;
+    uint32_t anye = 0;
 #pragma unroll
-    for (int k = 1; k <= 4; ++k) {
-        R.m[k] = u8_classify(R.w[k]);
-        const U8Masks &c = R.m[k], &p = R.m[k - 1];
+    for (int k = 0; k <= 4; ++k) {
         const uint32_t x = R.w[k];
-        const uint32_t must = fsl(p.L, c.L, 8) | fsl(p.E, c.E, 16) | fsl(p.F, c.F, 24);
-        det |= must ^ c.C;
-        // C0 / C1: 2-byte leads with payload bits 4..1 clear
-        det |= c.L & ~c.E & ~((x & 0x1E1E1E1Eu) + 0x7F7F7F7Fu);
-        // prefilter for E0 / ED (and EE / EF): E-class with low nibble in {0, D, E, F}
-        const uint32_t v = x + 0x03030303u;
-        pe |= c.E & ~(v << 4) & ~(v << 5);
-        anyf |= c.F;
+        const uint32_t t1 = x << 1;
+        R.m[k].C = x & ~t1 & H8;
+        R.m[k].L = x & t1 & H8;
+        R.m[k].E = R.m[k].L & (x << 2);
+        R.m[k].F = 0;
+        anye |= R.m[k].E;
     }
-    R.any4 = anyf;
-    if (__any_sync(0xffffffffu, (pe | anyf) != 0)) {
+    uint32_t det = 0;
+    if (!__any_sync(0xffffffffu, anye != 0)) {
+        R.path = 0;
 #pragma unroll
         for (int k = 1; k <= 4; ++k) {
             const U8Masks &c = R.m[k];
-            const uint32_t x = R.w[k];
-            const uint32_t n1 = fsr(x, R.w[k + 1], 8);
-            // E0 80..9F (overlong), ED A0..BF (surrogate): u = (b&0xF)<<1 | bit5(c1) in {0, 27}
-            const uint32_t u = ((x & 0x0F0F0F0Fu) << 1) | ((n1 >> 5) & 0x01010101u);
-            det |= c.E & ~c.F & ~((u + 0x7F7F7F7Fu) & ((u ^ 0x1B1B1B1Bu) + 0x7F7F7F7Fu));
-            // F0 80..8F (overlong), F4 90.. / F5..F7 (> U+10FFFF), F8..FF
-            const uint32_t key = ((x & 0x07070707u) << 2) | ((n1 >> 4) & 0x03030303u);
-            det |= c.F & (~(key + 0x7F7F7F7Fu) | (key + 0x6F6F6F6Fu) | (x << 4));
+            det |= fsl(R.m[k - 1].L, c.L, 8) ^ c.C;
+            det |= c.L & ~((R.w[k] & 0x1E1E1E1Eu) + 0x7F7F7F7Fu); // C0 / C1
+        }
+        R.det = det;
+        return;
+    }
+    uint32_t anyf = 0, any2 = 0;
+#pragma unroll
+    for (int k = 0; k <= 4; ++k) {
+        R.m[k].F = R.m[k].E & (R.w[k] << 3);
+        anyf |= R.m[k].F;
+        if (k > 0)
+            any2 |= R.m[k].L & ~R.m[k].E;
+    }
+    if (!__any_sync(0xffffffffu, (anyf | any2) != 0)) {
+        R.path = 1;
+        uint32_t pe = 0;
+#pragma unroll
+        for (int k = 1; k <= 4; ++k) {
+            const U8Masks &c = R.m[k], &p = R.m[k - 1];
+            det |= (fsl(p.L, c.L, 8) | fsl(p.E, c.E, 16)) ^ c.C;
+            pe |= u8_prefilter_e(R.w[k], c);
+        }
+        if (__any_sync(0xffffffffu, pe != 0)) {
+#pragma unroll
+            for (int k = 1; k <= 4; ++k)
+                det |= u8_check_e(R.w[k], fsr(R.w[k], R.w[k + 1], 8), R.m[k]);
+        }
+        R.det = det;
+        return;
+    }
+    R.path = 2;
+    uint32_t pe = 0;
+#pragma unroll
+    for (int k = 1; k <= 4; ++k) {
+        const U8Masks &c = R.m[k], &p = R.m[k - 1];
+        const uint32_t x = R.w[k];
+        det |= (fsl(p.L, c.L, 8) | fsl(p.E, c.E, 16) | fsl(p.F, c.F, 24)) ^ c.C;
+        det |= c.L & ~c.E & ~((x & 0x1E1E1E1Eu) + 0x7F7F7F7Fu); // C0 / C1
+        pe |= u8_prefilter_e(x, c);
+    }
+    if (__any_sync(0xffffffffu, (pe | anyf) != 0)) {
+#pragma unroll
+        for (int k = 1; k <= 4; ++k) {
+            const uint32_t n1 = fsr(R.w[k], R.w[k + 1], 8);
+            det |= u8_check_e(R.w[k], n1, R.m[k]) | u8_check_f(R.w[k], n1, R.m[k]);
         }
     }
     R.det = det;
@@ -210,6 +272,28 @@ __device__ __forceinline__ void u8_decode_quad(uint32_t x, uint32_t xn, const U8
         lo |= (lo4 & sF) | (lo3 & sS);
         hi |= (hi4 & sF) | (hiS & sS);
     }
+}
+
+// path 0: ASCII and 2-byte leads only
+__device__ __forceinline__ void u8_decode2(uint32_t x, uint32_t xn, uint32_t &lo, uint32_t &hi)
+{
+    const uint32_t n1 = fsr(x, xn, 8);
+    const uint32_t lo2 = ((x << 6) & 0xC0C0C0C0u) | (n1 & 0x3F3F3F3Fu);
+    const uint32_t sA = sgn8(x);
+    lo = (x & ~sA) | (lo2 & sA);
+    hi = (x >> 2) & 0x07070707u & sA;
+}
+
+// path 1: ASCII and 3-byte leads only
+__device__ __forceinline__ void u8_decode3(uint32_t x, uint32_t xn, uint32_t &lo, uint32_t &hi)
+{
+    const uint32_t n1 = fsr(x, xn, 8);
+    const uint32_t n2 = fsr(x, xn, 16);
+    const uint32_t lo3 = ((n1 << 6) & 0xC0C0C0C0u) | (n2 & 0x3F3F3F3Fu);
+    const uint32_t hi3 = ((x << 4) & 0xF0F0F0F0u) | ((n1 >> 2) & 0x0F0F0F0Fu);
+    const uint32_t sA = sgn8(x);
+    lo = (x & ~sA) | (lo3 & sA);
+    hi = hi3 & sA;
 }
 
 __device__ __forceinline__ void sts16(uint32_t addr, uint32_t v)
@@ -267,8 +351,13 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
         uint32_t e[4], fi1[4], c[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            fi1[k] = fsl(R.m[k].F, R.m[k + 1].F, 8);
-            e[k] = (~R.m[k + 1].C | fi1[k]) & H8;
+            if (R.path == 2) {
+                fi1[k] = fsl(R.m[k].F, R.m[k + 1].F, 8);
+                e[k] = (~R.m[k + 1].C | fi1[k]) & H8;
+            } else {
+                fi1[k] = 0;
+                e[k] = ~R.m[k + 1].C & H8;
+            }
             if (Boundary)
                 e[k] &= valid_mask(lane_off + 4 * k, lo_b, hi_b);
             c[k] = (uint32_t)__popc(e[k]);
@@ -342,13 +431,33 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
         }
 
         // decode + compact into the warp's staging region
-        const bool any4 = __any_sync(0xffffffffu, (R.any4 | R.m[0].F) != 0);
+        bool any4 = false;
+        if (R.path == 2) {
+            uint32_t f4 = R.m[0].F;
+#pragma unroll
+            for (int k = 1; k <= 4; ++k)
+                f4 |= R.m[k].F;
+            any4 = __any_sync(0xffffffffu, f4 != 0);
+        }
+        uint32_t lop[4], hip[4];
+        if (R.path == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                u8_decode2(R.w[k + 1], R.w[k + 2], lop[k], hip[k]);
+        } else if (R.path == 1) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                u8_decode3(R.w[k + 1], R.w[k + 2], lop[k], hip[k]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                u8_decode_quad(R.w[k + 1], R.w[k + 2], R.m[k + 1], fi1[k], any4, lop[k], hip[k]);
+        }
         uint32_t off = running + excl;
         const uint32_t lane_end = off + cnt;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            uint32_t lo, hi;
-            u8_decode_quad(R.w[k + 1], R.w[k + 2], R.m[k + 1], fi1[k], any4, lo, hi);
+            const uint32_t lo = lop[k], hi = hip[k];
             const uint32_t idx = (e[k] * 0x00204081u) >> 28;
             const SelPair sp = sel[idx];
             const uint32_t w01 = prmt(lo, hi, sp.s01);
