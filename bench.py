@@ -321,8 +321,11 @@ def main():
         }
     ncu = ncu_traffic()
     traffic = None
-    if ncu and "k_utf8_to_utf16le" in ncu:
-        traffic = ncu["k_utf8_to_utf16le"].get("dram_bytes_per_launch")
+    k1_key = "K1 utf8->utf16 (k_transcode<DirU8U16>)"
+    if ncu and k1_key in ncu:
+        # dram read+write bytes per launch, averaged over the same four
+        # 256 MiB profile buffers (tools/prof_kernels.py under ncu --set full)
+        traffic = round(ncu[k1_key]["dram_bytes_per_launch"])
 
     line = {
         "metric": METRIC,
@@ -352,8 +355,10 @@ def main():
             "unit": "GB/s",
             "frac": round(achieved / peak, 4),
             "traffic": traffic,
-            "kernel": "k_utf8_to_utf16le",
+            "kernel": "k_transcode<DirU8U16> (K1)",
             "algorithmic_bytes": "input bytes + 2 x written words, per launch",
+            "alg_bytes_per_launch": round(float(alg_bytes.mean())),
+            "traffic_source": "profiles/ncu_summary.json (ncu --set full, dram__bytes_read+write per launch)",
             "peak_source": peak_src,
             "per_profile": prof_detail,
         },

