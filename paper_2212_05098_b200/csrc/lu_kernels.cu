@@ -24,7 +24,7 @@ constexpr int kOutStrideU16 = kChunkBytes + 16;      // words per warp staging r
 constexpr int kOutStrideU8 = 3 * kChunkBytes / 2 + 32; // bytes per warp region (<= 3 bytes per word)
 
 constexpr size_t kInSmemBytes = sizeof(uint32_t) * kInWords;
-constexpr size_t kSmemK1 = 2 * sizeof(uint16_t) * kOutStrideU16 * kWarps; // double-buffered staging
+constexpr size_t kSmemK1 = 2 * sizeof(uint16_t) * kOutStrideU16 * kWarps; // 2 groups x 2 buffers x 4 warps
 constexpr size_t kSmemK2 = kInSmemBytes + kOutStrideU8 * kWarps;
 constexpr size_t kSmemVal = kInSmemBytes; // K4 (UTF-16) stages its tile; K3 reads registers
 
@@ -57,40 +57,37 @@ __device__ __forceinline__ void copy_out_u16(const uint16_t *src, uint32_t cnt, 
     // word offset r) in registers.
     const uint4 *s128 = reinterpret_cast<const uint4 *>(src);
     const uint32_t r = (8u - shift) & 7u;
-    for (uint32_t c = full_lo + lane; c < full_hi; c += 32) {
-        const uint32_t v = (8 * c - shift) >> 3;
-        const uint4 a = s128[v];
-        uint4 o;
-        if (r == 0) {
-            o = a;
-        } else {
-            const uint4 b = s128[v + 1];
-            const uint32_t w0 = a.x, w1 = a.y, w2 = a.z, w3 = a.w, w4 = b.x, w5 = b.y, w6 = b.z, w7 = b.w;
-            switch (r) {
-            case 1:
-                o = make_uint4(prmt(w0, w1, 0x5432), prmt(w1, w2, 0x5432), prmt(w2, w3, 0x5432), prmt(w3, w4, 0x5432));
-                break;
-            case 2:
-                o = make_uint4(w1, w2, w3, w4);
-                break;
-            case 3:
-                o = make_uint4(prmt(w1, w2, 0x5432), prmt(w2, w3, 0x5432), prmt(w3, w4, 0x5432), prmt(w4, w5, 0x5432));
-                break;
-            case 4:
-                o = make_uint4(w2, w3, w4, w5);
-                break;
-            case 5:
-                o = make_uint4(prmt(w2, w3, 0x5432), prmt(w3, w4, 0x5432), prmt(w4, w5, 0x5432), prmt(w5, w6, 0x5432));
-                break;
-            case 6:
-                o = make_uint4(w3, w4, w5, w6);
-                break;
-            default:
-                o = make_uint4(prmt(w3, w4, 0x5432), prmt(w4, w5, 0x5432), prmt(w5, w6, 0x5432), prmt(w6, w7, 0x5432));
-                break;
-            }
-        }
-        __stcs(reinterpret_cast<uint4 *>(dst) + c, o);
+    uint4 *d128 = reinterpret_cast<uint4 *>(dst);
+    // the word shift is warp-uniform: one specialised loop per value
+    switch (r) {
+    case 0:
+#pragma unroll 1
+        for (uint32_t c = full_lo + lane; c < full_hi; c += 32)
+            __stcs(d128 + c, s128[c]);
+        break;
+#define LU_COPY_CASE(R, BODY)                                                                                          \
+    case R:                                                                                                            \
+        _Pragma("unroll 1") for (uint32_t c = full_lo + lane; c < full_hi; c += 32) {                                  \
+            const uint32_t v = c - 1;                                                                                  \
+            const uint4 a = s128[v], b = s128[v + 1];                                                                  \
+            const uint32_t w0 = a.x, w1 = a.y, w2 = a.z, w3 = a.w, w4 = b.x, w5 = b.y, w6 = b.z, w7 = b.w;             \
+            (void)w0;                                                                                                  \
+            (void)w7;                                                                                                  \
+            __stcs(d128 + c, BODY);                                                                                    \
+        }                                                                                                              \
+        break;
+        LU_COPY_CASE(1, make_uint4(prmt(w0, w1, 0x5432), prmt(w1, w2, 0x5432), prmt(w2, w3, 0x5432),
+                                   prmt(w3, w4, 0x5432)))
+        LU_COPY_CASE(2, make_uint4(w1, w2, w3, w4))
+        LU_COPY_CASE(3, make_uint4(prmt(w1, w2, 0x5432), prmt(w2, w3, 0x5432), prmt(w3, w4, 0x5432),
+                                   prmt(w4, w5, 0x5432)))
+        LU_COPY_CASE(4, make_uint4(w2, w3, w4, w5))
+        LU_COPY_CASE(5, make_uint4(prmt(w2, w3, 0x5432), prmt(w3, w4, 0x5432), prmt(w4, w5, 0x5432),
+                                   prmt(w5, w6, 0x5432)))
+        LU_COPY_CASE(6, make_uint4(w3, w4, w5, w6))
+        LU_COPY_CASE(7, make_uint4(prmt(w3, w4, 0x5432), prmt(w4, w5, 0x5432), prmt(w5, w6, 0x5432),
+                                   prmt(w6, w7, 0x5432)))
+#undef LU_COPY_CASE
     }
     // partial chunks: head (chunk 0 when shift > 0) and tail (chunk full_hi)
     if (lane < 16) {
@@ -192,24 +189,31 @@ __device__ __forceinline__ void sel_table_init(SelPair *sel)
 
 // ====================================================== pipelined transcode
 //
-// Persistent CTAs (grid = resident capacity).  Warps 0..7 claim tiles from a
-// ticket counter just before computing them (so tiles finish roughly in
-// ticket order), compute each into one of two shared staging buffers and
-// publish the tile aggregate.  One extra warp in CTA 0 runs the central
-// scanner (scan_tiles) that turns aggregates into exclusive prefixes.  A
-// buffer is copied out when it is about to be reused, two tiles later, by
-// which time its prefix is normally known, so prefix latency hides behind
-// compute.  Every CTA is resident and a tile publishes its aggregate before
-// waiting on anything, so progress is guaranteed.
+// Persistent CTAs (grid = resident capacity).  A CTA holds two independent
+// tile groups of 4 compute warps each (8 KiB tiles) plus one extra warp that,
+// in CTA 0 only, runs the central scanner (scan_tiles).  Each group claims
+// tiles from a ticket counter just before computing them (tiles finish
+// roughly in ticket order), computes a tile into one of its two shared staging
+// buffers and publishes the tile aggregate; it copies a buffer out when it is
+// about to reuse it, two tiles later, by which time the scanner has normally
+// published that tile's exclusive prefix.  The two groups run unsynchronised,
+// so one group's HBM-bound copy-out overlaps the other's ALU-bound compute
+// (with a single 8-warp group the CTA alternated between the two phases and
+// they did not overlap).  Every CTA is resident and a tile publishes its
+// aggregate before waiting on anything, so progress is guaranteed.
 //
-// Named barriers (compute warps only, kThreads threads): 5 = ticket
-// broadcast, 6 = tile computed, 7 = prefix broadcast.
+// Named barriers per group g (kGroupThreads threads): 1+3g ticket broadcast,
+// 2+3g tile computed, 3+3g prefix broadcast.
 
-constexpr int kPipeThreads = kThreads + 32;
+constexpr int kGroupWarps = 4;
+constexpr int kGroupsPerCta = 2;
+constexpr int kGroupThreads = 32 * kGroupWarps;
+constexpr int kPipeTile = kGroupWarps * kChunkBytes; // 8 KiB
+constexpr int kPipeThreads = kGroupsPerCta * kGroupThreads + 32;
 
-struct PipeShared {
-    WarpResult wres[2][kWarps];
-    uint32_t warp_excl[2][kWarps];
+struct GroupShared {
+    WarpResult wres[2][kGroupWarps];
+    uint32_t warp_excl[2][kGroupWarps];
     uint64_t excl[2];
     uint32_t first_err[2];
     uint32_t tile_of[2];
@@ -228,9 +232,9 @@ struct DirU8U16 {
     static constexpr int kUnitShift = 0; // input positions are bytes
     template <bool B>
     __device__ static void compute(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, OutT *out_w,
-                                   const SelPair *sel, WarpResult &wr)
+                                   const SelPair *sel, WarpResult &wr, uint32_t wit)
     {
-        u8u16_warp<B>(base, tile_off, lo_b, hi_b, out_w, sel, wr);
+        u8u16_warp<B>(base, tile_off, lo_b, hi_b, out_w, sel, wr, wit);
     }
     __device__ static void copy_out(const OutT *src, uint32_t cnt, OutT *out_a, uint64_t g0)
     {
@@ -238,46 +242,51 @@ struct DirU8U16 {
     }
 };
 
+// Group thread 0: wait for the scanner's exclusive prefix of the tile held in
+// buffer b, and write the result record if this is the first-error tile or
+// the last tile.
 template <class Dir>
-__device__ __forceinline__ void pipe_copy_buffer(PipeShared &ps, uint32_t b, typename Dir::OutT *out_s,
-                                                 typename Dir::OutT *out_a, uint64_t out_lead, uint64_t *status,
-                                                 Outcome *res, uint32_t ntiles, int64_t lo_b, uint64_t n_units)
+__device__ __forceinline__ void pipe_resolve(GroupShared &ps, uint32_t b, uint64_t *status, Outcome *res,
+                                             uint32_t ntiles, int64_t lo_b, uint64_t n_units)
 {
-    const uint32_t warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {
-        const uint32_t tile = ps.tile_of[b];
-        uint64_t st = ld_acquire(&status[tile]);
-        while ((st >> kFlagShift) != 2) {
-            __nanosleep(32);
-            st = ld_acquire(&status[tile]);
-        }
-        const uint64_t ex = st & (kErrBit | kValMask);
-        ps.excl[b] = ex;
-        if (!(ex & kErrBit)) {
-            const uint32_t first = ps.first_err[b];
-            uint64_t units = 0;
-            for (uint32_t w = 0; w < kWarps && w <= first; ++w)
-                units += ps.wres[b][w].units;
-            const uint64_t written = ex + units;
-            const int64_t tile_off = (int64_t)tile * kTileBytes;
-            if (first < kWarps) {
-                res->status = kStatusMalformed;
-                res->pad = 0;
-                res->consumed = (uint64_t)((tile_off + ps.wres[b][first].pos - lo_b) >> Dir::kUnitShift);
-                res->written = written;
-            } else if (tile == ntiles - 1) {
-                res->status = kStatusOk;
-                res->pad = 0;
-                res->consumed = n_units;
-                res->written = written;
-            }
+    const uint32_t tile = ps.tile_of[b];
+    uint64_t st = ld_acquire(&status[tile]);
+    while ((st >> kFlagShift) != 2) {
+        __nanosleep(32);
+        st = ld_acquire(&status[tile]);
+    }
+    const uint64_t ex = st & (kErrBit | kValMask);
+    ps.excl[b] = ex;
+    if (!(ex & kErrBit)) {
+        const uint32_t first = ps.first_err[b];
+        uint64_t units = 0;
+        for (uint32_t w = 0; w < kGroupWarps && w <= first; ++w)
+            units += ps.wres[b][w].units;
+        const uint64_t written = ex + units;
+        const int64_t tile_off = (int64_t)tile * kPipeTile;
+        if (first < kGroupWarps) {
+            res->status = kStatusMalformed;
+            res->pad = 0;
+            res->consumed = (uint64_t)((tile_off + ps.wres[b][first].pos - lo_b) >> Dir::kUnitShift);
+            res->written = written;
+        } else if (tile == ntiles - 1) {
+            res->status = kStatusOk;
+            res->pad = 0;
+            res->consumed = n_units;
+            res->written = written;
         }
     }
-    bar_sync(7, kThreads);
+}
+
+// Every warp of the group: copy its staged region of buffer b out (prefix known).
+template <class Dir>
+__device__ __forceinline__ void pipe_copy(GroupShared &ps, uint32_t b, uint32_t wit, typename Dir::OutT *out_g,
+                                          typename Dir::OutT *out_a, uint64_t out_lead)
+{
     const uint64_t ex = ps.excl[b];
-    if (!(ex & kErrBit) && warp <= ps.first_err[b])
-        Dir::copy_out(out_s + (b * kWarps + warp) * Dir::kStride, ps.wres[b][warp].units, out_a,
-                      ex + ps.warp_excl[b][warp] + out_lead);
+    if (!(ex & kErrBit) && wit <= ps.first_err[b])
+        Dir::copy_out(out_g + (b * kGroupWarps + wit) * Dir::kStride, ps.wres[b][wit].units, out_a,
+                      ex + ps.warp_excl[b][wit] + out_lead);
 }
 
 template <class Dir>
@@ -288,43 +297,55 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
 {
     using OutT = typename Dir::OutT;
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    OutT *out_s = reinterpret_cast<OutT *>(smem_raw); // [2][kWarps][stride]
     __shared__ SelPair sel[16];
-    __shared__ PipeShared ps;
+    __shared__ GroupShared gshared[kGroupsPerCta];
 
     const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n_bytes;
     unsigned int *ticket = reinterpret_cast<unsigned int *>(status + ntiles);
     sel_table_init(sel);
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5;
-    if (warp == kWarps) {
+    if (warp == kGroupsPerCta * kGroupWarps) {
         if (blockIdx.x == 0)
             scan_tiles<16>(status, ntiles);
         return;
     }
+    const uint32_t g = warp / kGroupWarps, wit = warp % kGroupWarps;
+    const uint32_t gtid = threadIdx.x - g * kGroupThreads;
+    const uint32_t bar_claim = 1 + 3 * g, bar_done = 2 + 3 * g, bar_prefix = 3 + 3 * g;
+    GroupShared &ps = gshared[g];
+    OutT *out_g = reinterpret_cast<OutT *>(smem_raw) + g * (2 * kGroupWarps * Dir::kStride);
 
     uint32_t i = 0;
     for (;; ++i) {
         const uint32_t buf = i & 1;
-        if (i >= 2) // buffer reuse: copy out the tile computed two iterations ago
-            pipe_copy_buffer<Dir>(ps, buf, out_s, out_a, out_lead, status, res, ntiles, lo_b, n_units);
-        if (threadIdx.x == 0)
+        // one barrier publishes both this iteration's ticket and the prefix
+        // of the tile computed two iterations ago (buffer reuse)
+        // Claim at the top: a tile is computed right after it is claimed, so
+        // the scanner never waits on a claimed-but-idle tile (claiming one
+        // tile ahead measured 15% slower).
+        if (gtid == 0) {
+            if (i >= 2)
+                pipe_resolve<Dir>(ps, buf, status, res, ntiles, lo_b, n_units);
             ps.claim = atomicAdd(ticket, 1u);
-        bar_sync(5, kThreads);
+        }
+        bar_sync(bar_claim, kGroupThreads); // publishes ps.claim and, for i >= 2, ps.excl[buf]
+        if (i >= 2)
+            pipe_copy<Dir>(ps, buf, wit, out_g, out_a, out_lead);
         const uint32_t tile = ps.claim;
         if (tile >= ntiles)
             break;
-        const int64_t tile_off = (int64_t)tile * kTileBytes;
-        OutT *out_w = out_s + (buf * kWarps + warp) * Dir::kStride;
-        const bool interior = (tile_off - 4 >= lo_b) && (tile_off + kTileBytes + 4 <= hi_b);
+        const int64_t tile_off = (int64_t)tile * kPipeTile;
+        OutT *out_w = out_g + (buf * kGroupWarps + wit) * Dir::kStride;
+        const bool interior = (tile_off - 4 >= lo_b) && (tile_off + kPipeTile + 4 <= hi_b);
         if (interior)
-            Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][warp]);
+            Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit);
         else
-            Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][warp]);
-        bar_sync(6, kThreads);
-        if (threadIdx.x == 0) {
-            uint32_t units = 0, first = kWarps;
-            for (int w = 0; w < kWarps; ++w) {
+            Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit);
+        bar_sync(bar_done, kGroupThreads);
+        if (gtid == 0) {
+            uint32_t units = 0, first = kGroupWarps;
+            for (int w = 0; w < kGroupWarps; ++w) {
                 ps.warp_excl[buf][w] = units;
                 units += ps.wres[buf][w].units;
                 if (ps.wres[buf][w].err) {
@@ -334,12 +355,16 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
             }
             ps.first_err[buf] = first;
             ps.tile_of[buf] = tile;
-            st_release(&status[tile], kFlagAgg | (first < kWarps ? kErrBit : 0ull) | (uint64_t)units);
+            st_release(&status[tile], kFlagAgg | (first < kGroupWarps ? kErrBit : 0ull) | (uint64_t)units);
         }
     }
-    // drain: the last one or two tiles (in iteration order)
-    if (i >= 1)
-        pipe_copy_buffer<Dir>(ps, (i - 1) & 1, out_s, out_a, out_lead, status, res, ntiles, lo_b, n_units);
+    // drain the tile computed in the last iteration
+    if (i >= 1) {
+        if (gtid == 0)
+            pipe_resolve<Dir>(ps, (i - 1) & 1, status, res, ntiles, lo_b, n_units);
+        bar_sync(bar_prefix, kGroupThreads);
+        pipe_copy<Dir>(ps, (i - 1) & 1, wit, out_g, out_a, out_lead);
+    }
 }
 
 // ===================================================================== K2
@@ -427,9 +452,9 @@ __global__ void __launch_bounds__(kThreads) k_validate(const uint8_t *__restrict
         } else {
             const bool interior = (tile_off - 4 >= lo_b) && (tile_off + kTileBytes + 4 <= hi_b);
             if (interior)
-                u8val_warp<false>(base, tile_off, lo_b, hi_b, ts.wres[warp]);
+                u8val_warp<false>(base, tile_off, lo_b, hi_b, ts.wres[warp], warp);
             else
-                u8val_warp<true>(base, tile_off, lo_b, hi_b, ts.wres[warp]);
+                u8val_warp<true>(base, tile_off, lo_b, hi_b, ts.wres[warp], warp);
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -473,9 +498,9 @@ static int cuda_fail(cudaError_t e, const char *what)
     return LU_ERR_CUDA;
 }
 
-static uint64_t n_tiles(uint64_t bytes, uint32_t lead)
+static uint64_t n_tiles(uint64_t bytes, uint32_t lead, uint64_t tile = kTileBytes)
 {
-    uint64_t t = (bytes + lead + kTileBytes - 1) / kTileBytes;
+    uint64_t t = (bytes + lead + tile - 1) / tile;
     return t ? t : 1;
 }
 
@@ -533,7 +558,7 @@ uint64_t lu_workspace_bytes(int op, uint64_t n_units)
 {
     switch (op) {
     case LU_OP_UTF8_TO_UTF16LE:
-        return 8 * (n_tiles(n_units, 15) + 1) + 64;
+        return 8 * (n_tiles(n_units, 15, kPipeTile) + 1) + 64;
     case LU_OP_UTF16LE_TO_UTF8:
         return 8 * (n_tiles(2 * n_units, 15) + 1) + 64;
     case LU_OP_VALIDATE_UTF8:
@@ -566,7 +591,7 @@ int lu_utf8_to_utf16le(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint6
     if (!out && n_bytes)
         return fail(LU_ERR_INVALID, "null output");
     const uint32_t lead = (uint32_t)((uintptr_t)in & 15);
-    const uint64_t nt = n_tiles(n_bytes, lead);
+    const uint64_t nt = n_tiles(n_bytes, lead, kPipeTile);
     if (ws_bytes < 8 * (nt + 1)) // tile status words + the tile ticket counter
         return fail(LU_ERR_WORKSPACE, "workspace too small (see lu_workspace_bytes)");
     if (nt > 0x7fffffffull)

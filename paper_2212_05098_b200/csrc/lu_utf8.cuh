@@ -125,6 +125,15 @@ __device__ __forceinline__ uint32_t ld4(const uint8_t *base, int64_t a, int64_t 
     return load_u32_masked(base, a, lo, hi);
 }
 
+// 4-byte halo word; interior tiles are known to be in bounds
+template <bool Boundary>
+__device__ __forceinline__ uint32_t halo4(const uint8_t *base, int64_t a, int64_t lo, int64_t hi)
+{
+    if (!Boundary)
+        return __ldg(reinterpret_cast<const uint32_t *>(base + a));
+    return ld4(base, a, lo, hi);
+}
+
 struct WarpResult {
     uint32_t err;   // 1 if the warp's chunk holds the first bad unit of the tile
     uint32_t pos;   // tile-relative byte offset (aligned frame) of that unit
@@ -309,18 +318,18 @@ __device__ __forceinline__ void sts16_if(uint32_t addr, uint32_t v, uint32_t roo
 
 template <bool Boundary>
 __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
-                                           int64_t hi_b, uint16_t *out_w, const SelPair *sel, WarpResult &wr)
+                                           int64_t hi_b, uint16_t *out_w, const SelPair *sel, WarpResult &wr,
+                                           uint32_t warp /* warp index inside the tile */)
 {
     const uint32_t lane = lane_id();
-    const uint32_t warp = threadIdx.x >> 5;
     const int64_t chunk = tile_off + (int64_t)warp * kChunkBytes;
     constexpr int kRounds = kChunkBytes / 512;
     uint4 q[kRounds];
 #pragma unroll
     for (int r = 0; r < kRounds; ++r)
         q[r] = ld16(base, chunk + r * 512 + 16 * (int64_t)lane, lo_b, hi_b, Boundary);
-    uint32_t carry = (lane == 0) ? ld4(base, chunk - 4, lo_b, hi_b) : 0u;
-    const uint32_t halo_n = (lane == 31) ? ld4(base, chunk + kChunkBytes, lo_b, hi_b) : 0u;
+    uint32_t carry = (lane == 0) ? halo4<Boundary>(base, chunk - 4, lo_b, hi_b) : 0u;
+    const uint32_t halo_n = (lane == 31) ? halo4<Boundary>(base, chunk + kChunkBytes, lo_b, hi_b) : 0u;
     uint32_t rn[kRounds];
 #pragma unroll
     for (int r = 0; r < kRounds; ++r)
@@ -506,18 +515,17 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
 
 template <bool Boundary>
 __device__ __forceinline__ void u8val_warp(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
-                                           int64_t hi_b, WarpResult &wr)
+                                           int64_t hi_b, WarpResult &wr, uint32_t warp /* warp index in tile */)
 {
     const uint32_t lane = lane_id();
-    const uint32_t warp = threadIdx.x >> 5;
     const int64_t chunk = tile_off + (int64_t)warp * kChunkBytes;
     constexpr int kRounds = kChunkBytes / 512;
     uint4 q[kRounds];
 #pragma unroll
     for (int r = 0; r < kRounds; ++r)
         q[r] = ld16(base, chunk + r * 512 + 16 * (int64_t)lane, lo_b, hi_b, Boundary);
-    uint32_t carry = (lane == 0) ? ld4(base, chunk - 4, lo_b, hi_b) : 0u;
-    const uint32_t halo_n = (lane == 31) ? ld4(base, chunk + kChunkBytes, lo_b, hi_b) : 0u;
+    uint32_t carry = (lane == 0) ? halo4<Boundary>(base, chunk - 4, lo_b, hi_b) : 0u;
+    const uint32_t halo_n = (lane == 31) ? halo4<Boundary>(base, chunk + kChunkBytes, lo_b, hi_b) : 0u;
     uint32_t rn[kRounds];
 #pragma unroll
     for (int r = 0; r < kRounds; ++r)

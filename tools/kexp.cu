@@ -281,6 +281,71 @@ __global__ void __launch_bounds__(288, 3) kpipe(const uint8_t *base, uint64_t n,
     if (i >= 1) { nbar(6, 256); copy_buf((i - 1) & 1); }
 }
 
+template <int K, bool V2>
+__global__ void __launch_bounds__(288, 3) kpipe_t(const uint8_t *base, uint64_t n, uint16_t *out, uint64_t *status, uint32_t ntiles, unsigned long long *tm)
+{
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    uint16_t *out_s = reinterpret_cast<uint16_t *>(smem_raw); // [2][8][stride]
+    __shared__ SelPair sel[16];
+    __shared__ WarpResult wres[2][8];
+    __shared__ uint32_t wex[2][8], s_tile[2], s_claim;
+    __shared__ uint64_t s_excl[2];
+    unsigned int *ticket = reinterpret_cast<unsigned int *>(status + ntiles);
+    sel_init(sel);
+    __syncthreads();
+    const uint32_t warp = threadIdx.x >> 5;
+    if (warp == 8) { if (blockIdx.x == 0) scanner<K>(status, ntiles); return; }
+    auto copy_buf = [&](uint32_t b) {
+        if (threadIdx.x == 0) {
+            uint64_t st = ld_acquire(&status[s_tile[b]]);
+            while ((st >> kFlagShift) != 2) { __nanosleep(32); st = ld_acquire(&status[s_tile[b]]); }
+            s_excl[b] = st & (kErrBit | kValMask);
+        }
+        nbar(5, 256);
+        long long tc = clock64();
+        const uint64_t ex = s_excl[b];
+        if (!(ex & kErrBit)) {
+            if (V2) copy_out_u16_v2(out_s + (b * 8 + warp) * kOutStrideU16, wres[b][warp].units, out, ex + wex[b][warp]);
+            else copy_out_u16(out_s + (b * 8 + warp) * kOutStrideU16, wres[b][warp].units, out, ex + wex[b][warp]);
+        }
+        if (lane_id() == 0) atomicAdd(&tm[1], (unsigned long long)(clock64() - tc));
+    };
+    uint32_t i = 0;
+    for (;; ++i) {
+        const uint32_t buf = i & 1;
+        long long t0 = clock64();
+        if (i >= 2) copy_buf(buf);
+        long long t1 = clock64();
+        if (threadIdx.x == 0) s_claim = atomicAdd(ticket, 1u);
+        nbar(6, 256);
+        long long t2 = clock64();
+        const uint32_t tile = s_claim;
+        if (tile >= ntiles) break;
+        const int64_t tile_off = (int64_t)tile * kTileBytes;
+        uint16_t *out_w = out_s + (buf * 8 + warp) * kOutStrideU16;
+        const bool interior = (tile_off - 4 >= 0) && (tile_off + kTileBytes + 4 <= (int64_t)n);
+        if (interior) u8u16_warp<false>(base, tile_off, 0, n, out_w, sel, wres[buf][warp]);
+        else u8u16_warp<true>(base, tile_off, 0, n, out_w, sel, wres[buf][warp]);
+        long long t3 = clock64();
+        nbar(7, 256);
+        long long t4 = clock64();
+        if (lane_id() == 0) {
+            atomicAdd(&tm[0], (unsigned long long)(t1 - t0)); // copy phase incl. prefix wait
+            atomicAdd(&tm[2], (unsigned long long)(t2 - t1)); // claim
+            atomicAdd(&tm[3], (unsigned long long)(t3 - t2)); // compute
+            atomicAdd(&tm[4], (unsigned long long)(t4 - t3)); // barrier after compute
+            atomicAdd(&tm[5], 1ull);
+        }
+        if (threadIdx.x == 0) {
+            uint32_t acc = 0;
+            for (int w = 0; w < 8; ++w) { wex[buf][w] = acc; acc += wres[buf][w].units; }
+            s_tile[buf] = tile;
+            st_release(&status[tile], kFlagAgg | acc);
+        }
+    }
+    if (i >= 1) { nbar(6, 256); copy_buf((i - 1) & 1); }
+}
+
 // warp-specialized: 8 compute warps, 4 copy-out warps, 1 scanner warp (CTA 0)
 template <int K>
 __global__ void __launch_bounds__(416, 2) kpipe2(const uint8_t *base, uint64_t n, uint16_t *out, uint64_t *status, uint32_t ntiles)
@@ -431,6 +496,18 @@ int main(int argc, char **argv)
         rp("pipe scanner K8 copy-v1", kpipe<8, false>);
         rp("pipe scanner K16 copy-v1", kpipe<16, false>);
         rp("pipe scanner K16 copy-v2", kpipe<16, true>);
+        {
+            auto kern = kpipe_t<16, true>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            int per = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 288, sm);
+            unsigned long long *d_tm; cudaMalloc(&d_tm, 64); cudaMemset(d_tm, 0, 64);
+            cudaMemsetAsync(d_status, 0, 8 * (nt + 1));
+            kern<<<148 * per, 288, sm>>>(d_in, n, d_out, d_status, nt, d_tm);
+            unsigned long long tm[8]; cudaMemcpy(tm, d_tm, 64, cudaMemcpyDeviceToHost);
+            double c = (double)tm[5];
+            printf("   per warp-tile cycles: copy-phase %.0f (of which copy %.0f), claim %.0f, compute %.0f, post-compute barrier %.0f  (warp-tiles %llu)\n",
+                   tm[0] / c, tm[1] / c, tm[2] / c, tm[3] / c, tm[4] / c, tm[5]);
+        }
         {
             auto kern = kpipe2<16>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
