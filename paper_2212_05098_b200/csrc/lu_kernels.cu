@@ -25,7 +25,7 @@ constexpr int kOutStrideU8 = 3 * kChunkBytes / 2 + 32; // bytes per warp region 
 
 constexpr size_t kInSmemBytes = sizeof(uint32_t) * kInWords;
 constexpr size_t kSmemK1 = 2 * sizeof(uint16_t) * kOutStrideU16 * kWarps; // 2 groups x 2 buffers x 4 warps
-constexpr size_t kSmemK2 = kInSmemBytes + kOutStrideU8 * kWarps;
+constexpr size_t kSmemK2 = 2 * kOutStrideU8 * kWarps; // 2 groups x 2 buffers x 4 warps
 constexpr size_t kSmemVal = kInSmemBytes; // K4 (UTF-16) stages its tile; K3 reads registers
 
 struct TileShared {
@@ -239,6 +239,22 @@ struct DirU8U16 {
     __device__ static void copy_out(const OutT *src, uint32_t cnt, OutT *out_a, uint64_t g0)
     {
         copy_out_u16(src, cnt, out_a, g0);
+    }
+};
+
+struct DirU16U8 {
+    using OutT = uint8_t;
+    static constexpr int kStride = kOutStrideU8;
+    static constexpr int kUnitShift = 1; // input positions are 16-bit words
+    template <bool B>
+    __device__ static void compute(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, OutT *out_w,
+                                   const SelPair *, WarpResult &wr, uint32_t wit)
+    {
+        u16u8_warp_r<B>(base, tile_off, lo_b, hi_b, out_w, wr, wit);
+    }
+    __device__ static void copy_out(const OutT *src, uint32_t cnt, OutT *out_a, uint64_t g0)
+    {
+        copy_out_u8(src, cnt, out_a, g0);
     }
 };
 
@@ -512,7 +528,8 @@ static int set_smem_attrs()
         cudaError_t e;
         e = cudaFuncSetAttribute(k_transcode<DirU8U16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemK1);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_utf16le_to_utf8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemK2);
+            e = cudaFuncSetAttribute(k_transcode<DirU16U8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSmemK2);
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(k_validate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kSmemVal);
@@ -560,7 +577,7 @@ uint64_t lu_workspace_bytes(int op, uint64_t n_units)
     case LU_OP_UTF8_TO_UTF16LE:
         return 8 * (n_tiles(n_units, 15, kPipeTile) + 1) + 64;
     case LU_OP_UTF16LE_TO_UTF8:
-        return 8 * (n_tiles(2 * n_units, 15) + 1) + 64;
+        return 8 * (n_tiles(2 * n_units, 15, kPipeTile) + 1) + 64;
     case LU_OP_VALIDATE_UTF8:
     case LU_OP_VALIDATE_UTF16LE:
         return 64;
@@ -632,23 +649,27 @@ int lu_utf16le_to_utf8(const uint16_t *in, uint64_t n_words, uint8_t *out, uint6
         return fail(LU_ERR_INVALID, "null output");
     const uint8_t *inb = reinterpret_cast<const uint8_t *>(in);
     const uint32_t lead = (uint32_t)((uintptr_t)inb & 15);
-    const uint64_t nt = n_tiles(2 * n_words, lead);
-    if (ws_bytes < 8 * nt)
+    const uint64_t nt = n_tiles(2 * n_words, lead, kPipeTile);
+    if (ws_bytes < 8 * (nt + 1)) // tile status words + the tile ticket counter
         return fail(LU_ERR_WORKSPACE, "workspace too small (see lu_workspace_bytes)");
     if (nt > 0x7fffffffull)
         return fail(LU_ERR_INVALID, "input too large");
     int rc = set_smem_attrs();
     if (rc)
         return rc;
-    cudaError_t e = cudaMemsetAsync(ws, 0, 8 * nt, stream);
+    cudaError_t e = cudaMemsetAsync(ws, 0, 8 * (nt + 1), stream);
     if (e != cudaSuccess)
         return cuda_fail(e, "cudaMemsetAsync");
     const uint8_t *base = inb ? inb - lead : reinterpret_cast<const uint8_t *>(16);
     uint8_t *out_safe = out ? out : reinterpret_cast<uint8_t *>(16);
     const uint32_t out_lead = (uint32_t)((uintptr_t)out_safe & 15);
-    k_utf16le_to_utf8<<<(unsigned)nt, kThreads, kSmemK2, stream>>>(base, lead, n_words, out_safe - out_lead,
-                                                                   out_lead, reinterpret_cast<uint64_t *>(ws),
-                                                                   reinterpret_cast<Outcome *>(res), (uint32_t)nt);
+    unsigned grid = 0;
+    rc = persistent_grid((const void *)k_transcode<DirU16U8>, kPipeThreads, kSmemK2, nt, &grid);
+    if (rc)
+        return rc;
+    k_transcode<DirU16U8><<<grid, kPipeThreads, kSmemK2, stream>>>(
+        base, lead, n_words, 2 * n_words, out_safe - out_lead, out_lead, reinterpret_cast<uint64_t *>(ws),
+        reinterpret_cast<Outcome *>(res), (uint32_t)nt);
     e = cudaGetLastError();
     if (e != cudaSuccess)
         return cuda_fail(e, "k_utf16le_to_utf8 launch");

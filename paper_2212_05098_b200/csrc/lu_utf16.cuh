@@ -169,6 +169,174 @@ __device__ __forceinline__ void u16u8_warp(const uint32_t *in_s, uint8_t *out_w,
     }
 }
 
+__device__ __forceinline__ void sts8_if(uint32_t addr, uint32_t v, uint32_t n, uint32_t j)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.gt.u32 p, %2, %3;\n\t@p st.shared.u8 [%0], %1;\n\t}" ::"r"(addr),
+                 "r"(v), "r"(n), "r"(j)
+                 : "memory");
+}
+
+// K2 warp body for the pipelined kernel: the warp's 2 KiB chunk (1024 words)
+// in 4 rounds of 512 B, lane l holding words [8l, 8l+8) of the round in
+// registers; neighbour words by shuffle.  Per word: pair-aware UTF-8 encode
+// (u16_encode) and the exact local error predicate (u16_bad2); a warp-uniform
+// fast path skips the surrogate logic when a round has no surrogate.
+template <bool Boundary>
+__device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
+                                             int64_t hi_b, uint8_t *out_w, WarpResult &wr, uint32_t warp)
+{
+    const uint32_t lane = lane_id();
+    const int64_t chunk = tile_off + (int64_t)warp * kChunkBytes;
+    constexpr int kRounds = kChunkBytes / 512;
+    uint4 q[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t a = chunk + r * 512 + 16 * (int64_t)lane;
+        if (!Boundary)
+            q[r] = __ldcs(reinterpret_cast<const uint4 *>(base + a));
+        else if (a + 16 <= lo_b || a >= hi_b)
+            q[r] = make_uint4(0, 0, 0, 0);
+        else
+            q[r] = load_u128_masked(base, a, lo_b, hi_b);
+    }
+    uint32_t carry = 0, halo_n = 0;
+    if (lane == 0) {
+        const int64_t a = chunk - 4;
+        carry = Boundary ? ((a + 4 <= lo_b || a >= hi_b) ? 0u : load_u32_masked(base, a, lo_b, hi_b))
+                         : __ldg(reinterpret_cast<const uint32_t *>(base + a));
+    }
+    if (lane == 31) {
+        const int64_t a = chunk + kChunkBytes;
+        halo_n = Boundary ? ((a + 4 <= lo_b || a >= hi_b) ? 0u : load_u32_masked(base, a, lo_b, hi_b))
+                          : __ldg(reinterpret_cast<const uint32_t *>(base + a));
+    }
+    uint32_t rn[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r)
+        rn[r] = __shfl_sync(0xffffffffu, q[r].x, (lane + 1) & 31);
+
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(out_w);
+    uint32_t running = 0, err = 0, err_pos = 0, units = 0;
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t lane_off = chunk + r * 512 + 16 * (int64_t)lane;
+        const uint32_t rp = __shfl_sync(0xffffffffu, q[r].w, (lane + 31) & 31);
+        uint32_t w[6];
+        w[0] = (lane == 0) ? carry : rp;
+        carry = rp;
+        w[1] = q[r].x;
+        w[2] = q[r].y;
+        w[3] = q[r].z;
+        w[4] = q[r].w;
+        w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : halo_n) : rn[r];
+        uint32_t any = 0;
+#pragma unroll
+        for (int k = 1; k <= 4; ++k)
+            any |= u16_any_sur(w[k]) ? 1u : 0u;
+        any |= is_ls(w[5] & 0xFFFFu) ? 1u : 0u;
+        const bool sur = __any_sync(0xffffffffu, any != 0);
+        uint32_t lo[4], hi[4], n[4], bad[4];
+        uint32_t cnt = 0, anybad = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t x = w[k + 1];
+            const uint32_t w0 = x & 0xFFFFu, w1 = x >> 16, wp = w[k] >> 16, wn = w[k + 2] & 0xFFFFu;
+            uint32_t u0, l0, u1, l1;
+            if (sur) {
+                u16_encode(w0, wp, w1, u0, l0);
+                u16_encode(w1, w0, wn, u1, l1);
+                bad[k] = u16_bad2(w0, w1, wp, wn);
+            } else {
+                // no surrogates in the round: 1-3 bytes per word, never an error
+                u0 = w0 < 0x80u ? w0
+                     : w0 < 0x800u ? (0xC0u | (w0 >> 6)) | ((0x80u | (w0 & 0x3Fu)) << 8)
+                                   : (0xE0u | (w0 >> 12)) | ((0x80u | ((w0 >> 6) & 0x3Fu)) << 8) |
+                                         ((0x80u | (w0 & 0x3Fu)) << 16);
+                l0 = 1u + (w0 >= 0x80u) + (w0 >= 0x800u);
+                u1 = w1 < 0x80u ? w1
+                     : w1 < 0x800u ? (0xC0u | (w1 >> 6)) | ((0x80u | (w1 & 0x3Fu)) << 8)
+                                   : (0xE0u | (w1 >> 12)) | ((0x80u | ((w1 >> 6) & 0x3Fu)) << 8) |
+                                         ((0x80u | (w1 & 0x3Fu)) << 16);
+                l1 = 1u + (w1 >= 0x80u) + (w1 >= 0x800u);
+                bad[k] = 0;
+            }
+            if (Boundary) {
+                const uint32_t v = valid_words(lane_off + 4 * k, lo_b, hi_b);
+                if (!(v & 1))
+                    l0 = 0;
+                if (!(v & 2))
+                    l1 = 0;
+                bad[k] &= v;
+            }
+            // l0 <= 4 and u1 < 2^32, so the pair packs into 64 bits
+            const uint64_t p = (uint64_t)u0 | ((uint64_t)u1 << (8 * l0));
+            lo[k] = (uint32_t)p;
+            hi[k] = (uint32_t)(p >> 32);
+            n[k] = (l0 + l1) | (l0 << 8); // total bytes | bytes of the low word
+            cnt += l0 + l1;
+            anybad |= bad[k];
+        }
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= (uint32_t)d)
+                incl += o;
+        }
+        const uint32_t excl = incl - cnt;
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (sur && __any_sync(0xffffffffu, anybad != 0)) {
+            uint32_t kb = 8, within = excl;
+#pragma unroll
+            for (int k = 3; k >= 0; --k)
+                if (bad[k]) {
+                    const uint32_t which = (bad[k] & 1) ? 0u : 1u;
+                    kb = 2 * k + which;
+                }
+            // bytes emitted before the first bad word of this lane
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t nk = n[k] & 0xFFu, l0k = n[k] >> 8;
+                if ((uint32_t)(2 * k + 1) < kb)
+                    within += nk;
+                else if ((uint32_t)(2 * k) < kb)
+                    within += l0k;
+            }
+            const uint32_t bm = __ballot_sync(0xffffffffu, kb < 8);
+            const uint32_t fl = (uint32_t)__ffs(bm) - 1;
+            const uint32_t kbf = __shfl_sync(0xffffffffu, kb, fl);
+            const uint32_t wf = __shfl_sync(0xffffffffu, within, fl);
+            err = 1;
+            err_pos = (uint32_t)(chunk + r * 512 - tile_off) + 16 * fl + 2 * kbf;
+            units = running + wf;
+        }
+        uint32_t off = running + excl;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t a = sbase + off;
+            const uint32_t nk = n[k] & 0xFFu;
+            sts8_if(a, lo[k], nk, 0);
+            sts8_if(a + 1, lo[k] >> 8, nk, 1);
+            sts8_if(a + 2, lo[k] >> 16, nk, 2);
+            sts8_if(a + 3, lo[k] >> 24, nk, 3);
+            sts8_if(a + 4, hi[k], nk, 4);
+            sts8_if(a + 5, hi[k] >> 8, nk, 5);
+            sts8_if(a + 6, hi[k] >> 16, nk, 6);
+            off += nk;
+        }
+        running += tot;
+        if (err)
+            break;
+    }
+    if (!err)
+        units = running;
+    if (lane == 0) {
+        wr.err = err;
+        wr.pos = err_pos;
+        wr.units = units;
+    }
+}
+
 template <bool Boundary>
 __device__ __forceinline__ void u16val_warp(const uint32_t *in_s, int64_t tile_off, int64_t lo_b, int64_t hi_b,
                                             WarpResult &wr)
