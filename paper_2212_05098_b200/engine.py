@@ -33,8 +33,10 @@ from functools import lru_cache
 import numpy as np
 import torch
 
-from . import _native
+from . import _native, hostpipe
 from .outcome import STATUS_BY_CODE, TranscodeOutcome, TranscodeStatus
+
+_PIPELINE_MIN_BYTES = 8 << 20  # pinned host buffers at least this large use the chunked pipeline
 
 __all__ = [
     "UTF8_TO_UTF16",
@@ -320,6 +322,23 @@ def transcode(
     if direction == UTF16_TO_UTF8 and _byte_len(data) % 2:
         raise ValueError("UTF-16 input must be an even number of bytes")
     _require_native(kind)
+    if (
+        isinstance(data, torch.Tensor)
+        and isinstance(out, torch.Tensor)
+        and not data.is_cuda
+        and not out.is_cuda
+        and data.is_pinned()
+        and out.is_pinned()
+        and data.numel() * data.element_size() >= _PIPELINE_MIN_BYTES
+    ):
+        # pinned host in/out: chunked, overlapped H2D / kernel / D2H (hostpipe.py)
+        src = data.contiguous().view(torch.uint8).reshape(-1)
+        dst = out.view(torch.uint8).reshape(-1)
+        unit = 2 if direction == UTF8_TO_UTF16 else 1
+        cap = src.numel() if direction == UTF8_TO_UTF16 else 3 * (src.numel() // 2)
+        if dst.numel() < unit * cap:
+            raise ValueError("output buffer smaller than the worst case (worst_case_output_bytes)")
+        return hostpipe.pipelined_transcode(direction == UTF8_TO_UTF16, src, dst)
     device = _device()
     src = _to_device_bytes(data, device)
     out_dev = None

@@ -316,3 +316,44 @@ def test_each_utf16_error_kind(cuda_ok, kind):
         data = torch.from_numpy(base.copy())
         corpus.inject_errors(data, utf16=True, rate=2e-5, seed=600 + s, kinds=(kind,))
         check_u16(data.numpy().tobytes())
+
+
+# ------------------------------------------------ host-buffer pipeline (8f row 2)
+
+
+@pytest.mark.parametrize("utf16", [False, True])
+def test_pipelined_host_path(cuda_ok, utf16):
+    """Pinned host in/out through the chunked pipeline, small chunks, errors
+    placed in the middle chunk and right at chunk cuts; canary past written."""
+    from paper_2212_05098_b200 import hostpipe
+
+    units = 3_000_000
+    base = corpus.generate("mix", units, seed=31, utf16=utf16)
+    chunk = 256 << 10
+    cases = [None, 5, chunk - 1, chunk, 3 * chunk + 1, units // 2, units - 1]
+    for pos in cases:
+        data = base.clone()
+        if pos is not None:
+            if utf16:
+                data.view(torch.int16)[pos] = 0xDC00 - 0x10000
+            else:
+                data[pos] = 0xFF
+        host_in = data.pin_memory()
+        cap = 2 * units if not utf16 else 3 * units
+        host_out = torch.full((cap + 64,), 0xA5, dtype=torch.uint8).pin_memory()
+        got = hostpipe.pipelined_transcode(not utf16, host_in, host_out, chunk_bytes=chunk)
+        raw = data.numpy().tobytes()
+        ref, payload = oracle.utf16le_to_utf8(raw) if utf16 else oracle.utf8_to_utf16le(raw)
+        assert got.as_tuple() == ref, (pos, got, ref)
+        out = host_out.numpy()
+        assert out[: len(payload)].tobytes() == payload
+        assert (out[len(payload):] == 0xA5).all()
+
+
+def test_facade_routes_pinned_host_buffers(cuda_ok):
+    data = corpus.generate("cjk", 20 << 20, seed=32).pin_memory()
+    out = torch.empty(40 << 20, dtype=torch.uint8).pin_memory()
+    got = transcode(UTF8_TO_UTF16, data, out, engine="native")
+    ref, payload = oracle.utf8_to_utf16le(data.numpy())
+    assert got.as_tuple() == ref
+    assert out[: len(payload)].numpy().tobytes() == payload
