@@ -88,6 +88,9 @@ uint64_t lu_workspace_bytes(int op, uint64_t n_units);
 
 int lu_device_supported(int device);
 
+/* Input bytes per transcode tile (the unit the central scanner orders; the
+ * transcode workspace holds one 8-byte status word per tile).  Informational:
+ * callers never need to align anything to it. */
 int lu_tile_bytes(void);
 
 const char *lu_last_error(void);

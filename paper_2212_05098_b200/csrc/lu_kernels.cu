@@ -23,19 +23,8 @@ namespace lu {
 constexpr int kOutStrideU16 = kChunkBytes + 16;      // words per warp staging region (<= 1 word per byte)
 constexpr int kOutStrideU8 = 3 * kChunkBytes / 2 + 32; // bytes per warp region (<= 3 bytes per word)
 
-constexpr size_t kInSmemBytes = sizeof(uint32_t) * kInWords;
 constexpr size_t kSmemK1 = 2 * sizeof(uint16_t) * kOutStrideU16 * kWarps; // 2 groups x 2 buffers x 4 warps
 constexpr size_t kSmemK2 = 2 * kOutStrideU8 * kWarps; // 2 groups x 2 buffers x 4 warps
-constexpr size_t kSmemVal = kInSmemBytes; // K4 (UTF-16) stages its tile; K3 reads registers
-
-struct TileShared {
-    WarpResult wres[kWarps];
-    uint32_t warp_excl[kWarps];
-    uint64_t excl;
-    uint32_t first_err_warp;
-    uint32_t tile_units;
-    uint32_t skip;
-};
 
 // ------------------------------------------------------------- copy-out
 
@@ -139,34 +128,6 @@ __device__ __forceinline__ void copy_out_u8(const uint8_t *src, uint32_t cnt, ui
         if (i >= shift && i < total)
             dst[i] = src[i - shift];
     }
-}
-
-// ------------------------------------------------------- tile epilogue
-
-// Combine warp results (thread 0), look back (warp 0), broadcast.
-__device__ __forceinline__ void tile_scan(TileShared &ts, uint64_t *status)
-{
-    if (threadIdx.x == 0) {
-        uint32_t acc = 0, first = kWarps;
-        for (int w = 0; w < kWarps; ++w) {
-            ts.warp_excl[w] = acc;
-            acc += ts.wres[w].units;
-            if (ts.wres[w].err) {
-                first = (uint32_t)w;
-                break;
-            }
-        }
-        ts.first_err_warp = first;
-        ts.tile_units = acc;
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        const uint64_t agg = (ts.first_err_warp < kWarps ? kErrBit : 0ull) | (uint64_t)ts.tile_units;
-        const uint64_t ex = lookback(status, blockIdx.x, agg);
-        if (threadIdx.x == 0)
-            ts.excl = ex;
-    }
-    __syncthreads();
 }
 
 __device__ __forceinline__ void sel_table_init(SelPair *sel)
@@ -383,116 +344,70 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     }
 }
 
-// ===================================================================== K2
-
-__global__ void __launch_bounds__(kThreads) k_utf16le_to_utf8(const uint8_t *__restrict__ base, uint32_t lead,
-                                                               uint64_t n_words, uint8_t *__restrict__ out_a,
-                                                               uint32_t out_lead, uint64_t *__restrict__ status,
-                                                               Outcome *__restrict__ res, uint32_t ntiles)
-{
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    uint32_t *in_s = reinterpret_cast<uint32_t *>(smem_raw);
-    uint8_t *out_s = smem_raw + kInSmemBytes;
-    __shared__ TileShared ts;
-
-    const int64_t tile_off = (int64_t)blockIdx.x * kTileBytes;
-    const int64_t lo_b = lead, hi_b = (int64_t)lead + 2 * (int64_t)n_words;
-    const bool interior = stage_tile(in_s, base, tile_off, lo_b, hi_b);
-    __syncthreads();
-
-    const uint32_t warp = threadIdx.x >> 5;
-    uint8_t *out_w = out_s + warp * kOutStrideU8;
-    if (interior)
-        u16u8_warp<false>(in_s, out_w, tile_off, lo_b, hi_b, ts.wres[warp]);
-    else
-        u16u8_warp<true>(in_s, out_w, tile_off, lo_b, hi_b, ts.wres[warp]);
-    __syncthreads();
-    tile_scan(ts, status);
-
-    const uint64_t ex = ts.excl;
-    if (ex & kErrBit)
-        return;
-    const uint32_t first = ts.first_err_warp;
-    if (warp <= first && warp < kWarps) {
-        const uint64_t g0 = (ex & kValMask) + ts.warp_excl[warp] + out_lead;
-        copy_out_u8(out_w, ts.wres[warp].units, out_a, g0);
-    }
-    if (threadIdx.x == 0) {
-        const uint64_t written = (ex & kValMask) + ts.tile_units;
-        if (first < kWarps) {
-            res->status = kStatusMalformed;
-            res->pad = 0;
-            res->consumed = (uint64_t)((tile_off + ts.wres[first].pos - lo_b) >> 1);
-            res->written = written;
-        } else if (blockIdx.x == ntiles - 1) {
-            res->status = kStatusOk;
-            res->pad = 0;
-            res->consumed = n_words;
-            res->written = written;
-        }
-    }
-}
-
 // ================================================================= K3 / K4
+//
+// Warp-independent persistent validators: every warp walks 2 KiB chunks
+// (global warp id + i * total warps), with no CTA barrier and no staging.
+// A warp that finds an error publishes atomicMax(n - pos) and stops (its
+// later chunks all lie after the error); a warp also stops when a published
+// error lies before its next chunk (the reference stops at the first error
+// too).  The last warp to finish writes the result record.
+// ws layout: [u64 max(n - bad_pos)][u32 warps done][u32 pad].
 
-// ws layout for the validators: [u64 max(n - bad_pos)][u32 done][u32 pad]
 template <bool Utf16>
-__global__ void __launch_bounds__(kThreads) k_validate(const uint8_t *__restrict__ base, uint32_t lead, uint64_t n,
-                                                       uint64_t *__restrict__ ws, Outcome *__restrict__ res,
-                                                       uint32_t ntiles)
+__global__ void __launch_bounds__(kThreads) k_validate_w(const uint8_t *__restrict__ base, uint32_t lead,
+                                                         uint64_t n, uint64_t *__restrict__ ws,
+                                                         Outcome *__restrict__ res, uint64_t nchunks)
 {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    uint32_t *in_s = reinterpret_cast<uint32_t *>(smem_raw);
-    __shared__ TileShared ts;
+    __shared__ WarpResult wr_s[kWarps];
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t lane = lane_id();
+    const uint64_t total_warps = (uint64_t)gridDim.x * kWarps;
     const uint64_t n_bytes = Utf16 ? 2 * n : n;
-    const int64_t tile_off = (int64_t)blockIdx.x * kTileBytes;
     const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n_bytes;
-
-    if (threadIdx.x == 0) {
-        // a tile that starts after an already-found error has nothing to
-        // decide (the reference stops at the first error too)
-        const uint64_t best = *reinterpret_cast<volatile uint64_t *>(ws);
-        const int64_t bad_b = lo_b + (Utf16 ? 2 : 1) * (int64_t)(n - best);
-        ts.skip = best != 0 && bad_b < tile_off;
-    }
-    __syncthreads();
-    if (!ts.skip) {
-        const uint32_t warp = threadIdx.x >> 5;
+    uint64_t best = 0; // cached global max(n - bad_pos)
+    // (a cp.async double buffer per warp measured 6-11% slower: the loads are
+    // already latency-hidden by 32 resident warps per SM)
+    for (uint64_t c = (uint64_t)blockIdx.x * kWarps + warp; c < nchunks; c += total_warps) {
+        const int64_t off = (int64_t)c * kChunkBytes;
+        if (best != 0 && lo_b + (Utf16 ? 2 : 1) * (int64_t)(n - best) < off)
+            break; // an earlier error is already known
+        const uint64_t best_next = *reinterpret_cast<volatile uint64_t *>(ws); // consumed next iteration
+        const bool interior = (off - 4 >= lo_b) && (off + kChunkBytes + 4 <= hi_b);
+        uint32_t err, pos;
         if (Utf16) {
-            const bool interior = stage_tile(in_s, base, tile_off, lo_b, hi_b);
-            __syncthreads();
             if (interior)
-                u16val_warp<false>(in_s, tile_off, lo_b, hi_b, ts.wres[warp]);
+                u16val_warp_r<false>(base, off, lo_b, hi_b, err, pos);
             else
-                u16val_warp<true>(in_s, tile_off, lo_b, hi_b, ts.wres[warp]);
+                u16val_warp_r<true>(base, off, lo_b, hi_b, err, pos);
         } else {
-            const bool interior = (tile_off - 4 >= lo_b) && (tile_off + kTileBytes + 4 <= hi_b);
             if (interior)
-                u8val_warp<false>(base, tile_off, lo_b, hi_b, ts.wres[warp], warp);
+                u8val_warp<false>(base, off, lo_b, hi_b, wr_s[warp], 0);
             else
-                u8val_warp<true>(base, tile_off, lo_b, hi_b, ts.wres[warp], warp);
+                u8val_warp<true>(base, off, lo_b, hi_b, wr_s[warp], 0);
+            __syncwarp();
+            err = wr_s[warp].err;
+            pos = wr_s[warp].pos;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            for (int w = 0; w < kWarps; ++w) {
-                if (ts.wres[w].err) {
-                    const int64_t pb = tile_off + ts.wres[w].pos - lo_b; // byte position
-                    const uint64_t pu = Utf16 ? (uint64_t)(pb >> 1) : (uint64_t)pb;
-                    atomicMax(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)(n - pu));
-                    break;
-                }
+        if (err) {
+            if (lane == 0) {
+                const int64_t pb = off + pos - lo_b;
+                const uint64_t pu = Utf16 ? (uint64_t)(pb >> 1) : (uint64_t)pb;
+                atomicMax(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)(n - pu));
             }
+            break;
         }
+        best = best_next;
     }
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
         __threadfence();
-        const uint32_t prev = atomicAdd(reinterpret_cast<unsigned int *>(ws + 1), 1u);
-        if (prev == ntiles - 1) {
+        const unsigned int prev = atomicAdd(reinterpret_cast<unsigned int *>(ws + 1), 1u);
+        if (prev == total_warps - 1) {
             __threadfence();
-            const uint64_t best = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 0ull);
-            res->status = best ? kStatusMalformed : kStatusOk;
+            const uint64_t b = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 0ull);
+            res->status = b ? kStatusMalformed : kStatusOk;
             res->pad = 0;
-            res->consumed = n - best;
+            res->consumed = n - b;
             res->written = 0;
         }
     }
@@ -530,11 +445,6 @@ static int set_smem_attrs()
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(k_transcode<DirU16U8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kSmemK2);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_validate<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kSmemVal);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_validate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemVal);
         status = e;
     });
     if (status != cudaSuccess)
@@ -594,7 +504,7 @@ int lu_device_supported(int dev)
     return p.major == 10 && p.minor == 0;
 }
 
-int lu_tile_bytes(void) { return kTileBytes; }
+int lu_tile_bytes(void) { return kPipeTile; }
 
 int lu_utf8_to_utf16le(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint64_t out_cap_words, void *ws,
                        uint64_t ws_bytes, lu_outcome *res, cudaStream_t stream)
@@ -696,12 +606,18 @@ static int validate_impl(bool utf16, const uint8_t *inb, uint64_t n_units, void 
     if (e != cudaSuccess)
         return cuda_fail(e, "cudaMemsetAsync");
     const uint8_t *base = inb ? inb - lead : reinterpret_cast<const uint8_t *>(16);
+    const uint64_t nchunks = n_tiles(utf16 ? 2 * n_units : n_units, lead, kChunkBytes);
+    unsigned grid = 0;
+    rc = persistent_grid(utf16 ? (const void *)k_validate_w<true> : (const void *)k_validate_w<false>, kThreads, 0,
+                         (nchunks + kWarps - 1) / kWarps, &grid);
+    if (rc)
+        return rc;
     if (utf16)
-        k_validate<true><<<(unsigned)nt, kThreads, kSmemVal, stream>>>(
-            base, lead, n_units, reinterpret_cast<uint64_t *>(ws), reinterpret_cast<Outcome *>(res), (uint32_t)nt);
+        k_validate_w<true><<<grid, kThreads, 0, stream>>>(base, lead, n_units, reinterpret_cast<uint64_t *>(ws),
+                                                          reinterpret_cast<Outcome *>(res), nchunks);
     else
-        k_validate<false><<<(unsigned)nt, kThreads, kSmemVal, stream>>>(
-            base, lead, n_units, reinterpret_cast<uint64_t *>(ws), reinterpret_cast<Outcome *>(res), (uint32_t)nt);
+        k_validate_w<false><<<grid, kThreads, 0, stream>>>(base, lead, n_units, reinterpret_cast<uint64_t *>(ws),
+                                                           reinterpret_cast<Outcome *>(res), nchunks);
     e = cudaGetLastError();
     if (e != cudaSuccess)
         return cuda_fail(e, "k_validate launch");

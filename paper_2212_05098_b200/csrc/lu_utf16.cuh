@@ -65,110 +65,6 @@ __device__ __forceinline__ uint32_t valid_words(int64_t a, int64_t lo, int64_t h
     return (uint32_t)(a >= lo && a + 2 <= hi) | ((uint32_t)(a + 2 >= lo && a + 4 <= hi) << 1);
 }
 
-template <bool Boundary>
-__device__ __forceinline__ void u16u8_warp(const uint32_t *in_s, uint8_t *out_w, int64_t tile_off, int64_t lo_b,
-                                           int64_t hi_b, WarpResult &wr)
-{
-    const uint32_t lane = lane_id();
-    const uint32_t warp = threadIdx.x >> 5;
-    const int q0 = kInHead + (int)warp * kChunkQuads;
-    uint32_t running = 0;
-    uint32_t err = 0, err_pos = 0, units = 0;
-
-#pragma unroll 1
-    for (int g = 0; g < kGroups; ++g) {
-        uint32_t u0[kGroup], u1[kGroup], l0[kGroup], l1[kGroup], bad[kGroup];
-        uint32_t pk = 0, anybad = 0;
-        const int qg = q0 + g * kGroup * 32;
-#pragma unroll
-        for (int j = 0; j < kGroup; ++j) {
-            const int q = qg + j * 32 + (int)lane;
-            const uint32_t x = in_s[q];
-            const uint32_t xp = in_s[q - 1];
-            const uint32_t xn = in_s[q + 1];
-            const uint32_t w0 = x & 0xFFFFu, w1 = x >> 16, wp = xp >> 16, wn = xn & 0xFFFFu;
-            u16_encode(w0, wp, w1, u0[j], l0[j]);
-            u16_encode(w1, w0, wn, u1[j], l1[j]);
-            bad[j] = 0;
-            if (__any_sync(0xffffffffu, u16_any_sur(x) || is_ls(wn)))
-                bad[j] = u16_bad2(w0, w1, wp, wn);
-            if (Boundary) {
-                const int64_t a = tile_off + 4 * (int64_t)(q - kInHead);
-                const uint32_t v = valid_words(a, lo_b, hi_b);
-                if (!(v & 1))
-                    l0[j] = 0;
-                if (!(v & 2))
-                    l1[j] = 0;
-                bad[j] &= v;
-            }
-            anybad |= bad[j];
-            pk |= (l0[j] + l1[j]) << (8 * j);
-        }
-        const uint32_t incl = warp_scan_packed(pk);
-        const uint32_t excl = incl - pk;
-        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-
-        if (__any_sync(0xffffffffu, anybad != 0)) {
-            uint32_t before = running;
-            bool found = false;
-#pragma unroll
-            for (int j = 0; j < kGroup; ++j) {
-                if (!found) {
-                    const uint32_t bm = __ballot_sync(0xffffffffu, bad[j] != 0);
-                    if (bm) {
-                        const uint32_t fl = (uint32_t)__ffs(bm) - 1;
-                        const uint32_t which = (bad[j] & 1) ? 0u : 1u;
-                        const uint32_t within = ((excl >> (8 * j)) & 0xFFu) + (which ? l0[j] : 0u);
-                        const uint32_t wf = __shfl_sync(0xffffffffu, within, fl);
-                        const uint32_t whf = __shfl_sync(0xffffffffu, which, fl);
-                        err = 1;
-                        // tile-relative byte offset of the bad word
-                        err_pos = 4u * (uint32_t)(qg + j * 32 + (int)fl - kInHead) + 2u * whf;
-                        units = before + wf;
-                        found = true;
-                    }
-                }
-                before += (tot >> (8 * j)) & 0xFFu;
-            }
-        }
-
-        uint32_t base = running;
-#pragma unroll
-        for (int j = 0; j < kGroup; ++j) {
-            const uint32_t off = base + ((excl >> (8 * j)) & 0xFFu);
-            const uint64_t p = (uint64_t)u0[j] | ((uint64_t)u1[j] << (8 * l0[j]));
-            const uint32_t pl = (uint32_t)p, ph = (uint32_t)(p >> 32);
-            const uint32_t n = l0[j] + l1[j];
-            uint8_t *dst = out_w + off;
-            if (n > 0)
-                dst[0] = (uint8_t)pl;
-            if (n > 1)
-                dst[1] = (uint8_t)(pl >> 8);
-            if (n > 2)
-                dst[2] = (uint8_t)(pl >> 16);
-            if (n > 3)
-                dst[3] = (uint8_t)(pl >> 24);
-            if (n > 4)
-                dst[4] = (uint8_t)ph;
-            if (n > 5)
-                dst[5] = (uint8_t)(ph >> 8);
-            if (n > 6)
-                dst[6] = (uint8_t)(ph >> 16);
-            base += (tot >> (8 * j)) & 0xFFu;
-        }
-        running = base;
-        if (err)
-            break;
-    }
-    if (!err)
-        units = running;
-    if (lane == 0) {
-        wr.err = err;
-        wr.pos = err_pos;
-        wr.units = units;
-    }
-}
-
 __device__ __forceinline__ void sts8_if(uint32_t addr, uint32_t v, uint32_t n, uint32_t j)
 {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.gt.u32 p, %2, %3;\n\t@p st.shared.u8 [%0], %1;\n\t}" ::"r"(addr),
@@ -337,39 +233,97 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
     }
 }
 
+// SWAR surrogate masks of a quad (two words): bit 15 / 31 set for a high
+// (resp. low) surrogate.
+__device__ __forceinline__ void u16_sur_masks(uint32_t x, uint32_t &hs, uint32_t &ls)
+{
+    const uint32_t a = (x & 0xFC00FC00u) ^ 0xD800D800u; // 0 for a high surrogate, 0x0400 for a low one
+    const uint32_t b = a ^ 0x04000400u;
+    // bit 15 of each half set iff that half is nonzero (exact; no carry between halves)
+    const uint32_t nza = ((a & 0x7FFF7FFFu) + 0x7FFF7FFFu) | a;
+    const uint32_t nzb = ((b & 0x7FFF7FFFu) + 0x7FFF7FFFu) | b;
+    hs = ~nza & 0x80008000u;
+    ls = ~nzb & 0x80008000u;
+}
+
+// K4 warp body: validate one 2 KiB chunk (1024 words) in 4 rounds of 512 B,
+// lane l holding words [8l, 8l+8) in registers.  A low surrogate must sit
+// exactly where the previous word is a high surrogate, so the round is clean
+// iff ls == hs shifted by one word (one funnel shift per quad); a flagged
+// round is resolved with the exact predicate u16_bad2.
 template <bool Boundary>
-__device__ __forceinline__ void u16val_warp(const uint32_t *in_s, int64_t tile_off, int64_t lo_b, int64_t hi_b,
-                                            WarpResult &wr)
+__device__ __forceinline__ void u16val_warp_r(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
+                                              int64_t hi_b, uint32_t &err, uint32_t &err_pos)
 {
     const uint32_t lane = lane_id();
-    const uint32_t warp = threadIdx.x >> 5;
-    const int q0 = kInHead + (int)warp * kChunkQuads;
-    uint32_t err = 0, err_pos = 0;
-#pragma unroll 4
-    for (int s = 0; s < kSteps; ++s) {
-        const int q = q0 + s * 32 + (int)lane;
-        const uint32_t x = in_s[q];
-        const uint32_t xn = in_s[q + 1];
-        uint32_t bad = 0;
-        if (__any_sync(0xffffffffu, u16_any_sur(x) || is_ls(xn & 0xFFFFu))) {
-            const uint32_t xp = in_s[q - 1];
-            bad = u16_bad2(x & 0xFFFFu, x >> 16, xp >> 16, xn & 0xFFFFu);
-            if (Boundary)
-                bad &= valid_words(tile_off + 4 * (int64_t)(q - kInHead), lo_b, hi_b);
-        }
-        const uint32_t bm = __ballot_sync(0xffffffffu, bad != 0);
-        if (bm) {
-            const uint32_t fl = (uint32_t)__ffs(bm) - 1;
-            const uint32_t which = __shfl_sync(0xffffffffu, (bad & 1) ? 0u : 1u, fl);
-            err = 1;
-            err_pos = 4u * (uint32_t)(q0 + s * 32 + (int)fl - kInHead) + 2u * which;
-            break;
-        }
+    const int64_t chunk = tile_off;
+    constexpr int kRounds = kChunkBytes / 512;
+    uint4 q[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t a = chunk + r * 512 + 16 * (int64_t)lane;
+        if (!Boundary)
+            q[r] = __ldcs(reinterpret_cast<const uint4 *>(base + a));
+        else if (a + 16 <= lo_b || a >= hi_b)
+            q[r] = make_uint4(0, 0, 0, 0);
+        else
+            q[r] = load_u128_masked(base, a, lo_b, hi_b);
     }
+    uint32_t carry = 0, halo_n = 0;
     if (lane == 0) {
-        wr.err = err;
-        wr.pos = err_pos;
-        wr.units = 0;
+        const int64_t a = chunk - 4;
+        carry = Boundary ? ((a + 4 <= lo_b || a >= hi_b) ? 0u : load_u32_masked(base, a, lo_b, hi_b))
+                         : __ldg(reinterpret_cast<const uint32_t *>(base + a));
+    }
+    if (lane == 31) {
+        const int64_t a = chunk + kChunkBytes;
+        halo_n = Boundary ? ((a + 4 <= lo_b || a >= hi_b) ? 0u : load_u32_masked(base, a, lo_b, hi_b))
+                          : __ldg(reinterpret_cast<const uint32_t *>(base + a));
+    }
+    uint32_t rn[kRounds];
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r)
+        rn[r] = __shfl_sync(0xffffffffu, q[r].x, (lane + 1) & 31);
+    err = 0;
+    err_pos = 0;
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const uint32_t rp = __shfl_sync(0xffffffffu, q[r].w, (lane + 31) & 31);
+        uint32_t w[6];
+        w[0] = (lane == 0) ? carry : rp;
+        carry = rp;
+        w[1] = q[r].x;
+        w[2] = q[r].y;
+        w[3] = q[r].z;
+        w[4] = q[r].w;
+        w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : halo_n) : rn[r];
+        uint32_t hs[6], ls[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k)
+            u16_sur_masks(w[k], hs[k], ls[k]);
+        uint32_t det = 0;
+#pragma unroll
+        for (int k = 1; k <= 5; ++k)
+            det |= ls[k] ^ fsl(hs[k - 1], hs[k], 16);
+        if (__any_sync(0xffffffffu, det != 0)) {
+            const int64_t lane_off = chunk + r * 512 + 16 * (int64_t)lane;
+            uint32_t kb = 8;
+#pragma unroll
+            for (int k = 3; k >= 0; --k) {
+                uint32_t b = u16_bad2(w[k + 1] & 0xFFFFu, w[k + 1] >> 16, w[k] >> 16, w[k + 2] & 0xFFFFu);
+                if (Boundary)
+                    b &= valid_words(lane_off + 4 * k, lo_b, hi_b);
+                if (b)
+                    kb = 2 * k + ((b & 1) ? 0u : 1u);
+            }
+            const uint32_t bm = __ballot_sync(0xffffffffu, kb < 8);
+            if (bm) {
+                const uint32_t fl = (uint32_t)__ffs(bm) - 1;
+                err = 1;
+                err_pos = (uint32_t)(r * 512) + 16 * fl + 2 * __shfl_sync(0xffffffffu, kb, fl);
+                return;
+            }
+        }
     }
 }
 

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 def test_host_only_calls():
     lib = _native.lib()
     assert lib.lu_version().startswith(b"laneutf_b200")
-    assert lib.lu_tile_bytes() == 16384
+    assert lib.lu_tile_bytes() == 8192
     assert _native.workspace_bytes(_native.OP_UTF8_TO_UTF16LE, 1 << 20) >= 8 * 64
     assert _native.workspace_bytes(_native.OP_VALIDATE_UTF8, 1 << 30) >= 16
     assert _native.workspace_bytes(99, 10) == 0
