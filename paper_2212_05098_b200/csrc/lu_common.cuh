@@ -94,63 +94,139 @@ __device__ __forceinline__ uint64_t seq_combine(uint64_t a, uint64_t b)
     return (b & kErrBit) | (((a & kValMask) + (b & kValMask)) & kValMask);
 }
 
-// Central scanner, run by one warp for the whole grid.  Tiles publish only
-// their aggregate (flag 1); the scanner sweeps the status array in tile order,
-// 32*K entries per pass, and replaces each ready entry by flag 2 | EXCLUSIVE
-// prefix.  One pass covers up to 32*K tiles per L2 round trip, and no tile
-// ever waits on an inclusive-prefix chain: a tile's owner just polls its own
-// status word.  It stops at the first tile whose aggregate is not yet
-// published, so every claimed tile must publish without waiting on anything.
-template <int K>
-__device__ __forceinline__ void scan_tiles(uint64_t *status, uint32_t ntiles)
+// Optional phase profiler (make prof -> liblaneutf_b200_prof.so; never the
+// shipped library): per-phase SM clock cycles summed over groups.
+#ifdef LU_PROF
+__device__ unsigned long long g_prof[48];
+__shared__ unsigned long long s_prof[10][24]; // [warp][counter], lane 0 only
+#define LU_T0() long long _t0 = clock64()
+#define LU_T(k)                                                                       \
+    do {                                                                              \
+        const long long _t1 = clock64();                                              \
+        if ((threadIdx.x & 31) == 0)                                                  \
+            s_prof[threadIdx.x >> 5][k] += (unsigned long long)(_t1 - _t0);           \
+        _t0 = _t1;                                                                    \
+    } while (0)
+#define LU_CNT(k, v)                                                                  \
+    do {                                                                              \
+        if ((threadIdx.x & 31) == 0)                                                  \
+            s_prof[threadIdx.x >> 5][k] += (unsigned long long)(v);                   \
+    } while (0)
+#define LU_PROF_INIT()                                                                \
+    do {                                                                              \
+        if ((threadIdx.x & 31) == 0)                                                  \
+            for (int _k = 0; _k < 24; ++_k)                                           \
+                s_prof[threadIdx.x >> 5][_k] = 0;                                     \
+    } while (0)
+#define LU_PROF_FLUSH()                                                               \
+    do {                                                                              \
+        if ((threadIdx.x & 31) == 0)                                                  \
+            for (int _k = 0; _k < 24; ++_k)                                           \
+                atomicAdd(&g_prof[_k + ((threadIdx.x >> 5) % 4 ? 24 : 0)], s_prof[threadIdx.x >> 5][_k]);                 \
+    } while (0)
+#else
+#define LU_T0()
+#define LU_T(k)
+#define LU_CNT(k, v)
+#define LU_PROF_INIT()
+#define LU_PROF_FLUSH()
+#endif
+
+// Central scanner: the kScanWarps warps of CTA 0 (which computes no tiles).
+// Tiles publish only their aggregate (flag 1).  Scanner warp k owns the
+// fixed windows k, k + kScanWarps, ... of kScanWindow tiles: it polls until
+// every tile of its window has published, scans the window locally (lane l
+// holds tiles [4l, 4l+4)), takes the window base from the previous window's
+// warp through shared memory, hands on its own end value, and replaces each
+// entry by flag 2 | EXCLUSIVE prefix.  Only the base hand-off is serial; the
+// polling, local scans and stores of kScanWarps windows proceed in parallel
+// (one warp sweeping serially was the throughput limit: ~3 us per pass).
+// A tile's owner just polls its own status word.
+//
+// Errors: the count of a tile at or after the first malformed tile is never
+// used (nothing there is copied out), so a prefix is the plain sum of the
+// preceding counts, with the error bit set iff some preceding tile is
+// malformed.
+constexpr int kScanWarps = 8;
+constexpr int kScanPerLane = 4;
+constexpr uint32_t kScanWindow = 32 * kScanPerLane; // 128 tiles
+
+struct ScanShared {
+    unsigned long long base[kScanWarps]; // end value of the window in the slot
+    uint32_t tag[kScanWarps];            // window index + 1 once base is valid
+};
+
+__device__ __forceinline__ void scan_init(ScanShared &ss)
+{
+    if (threadIdx.x < kScanWarps)
+        ss.tag[threadIdx.x] = 0;
+}
+
+__device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, uint32_t sw, ScanShared &ss)
 {
     const uint32_t lane = lane_id();
-    uint32_t next = 0;
-    uint64_t acc = 0;
-    while (next < ntiles) {
-        uint64_t s[K];
+    const uint32_t nwin = (ntiles + kScanWindow - 1) / kScanWindow;
+    volatile unsigned long long *vbase = ss.base;
+    volatile uint32_t *vtag = ss.tag;
+    for (uint32_t w = sw; w < nwin; w += kScanWarps) {
+        const uint32_t t0 = w * kScanWindow + lane * kScanPerLane;
+        uint64_t s[kScanPerLane];
+        uint32_t have = 0; // bit j: s[j] holds a published aggregate
+        for (;;) {
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const uint32_t t = next + lane * K + j;
-            s[j] = t < ntiles ? ld_acquire(&status[t]) : 0ull;
-        }
-        uint32_t r = K; // leading ready entries of this lane's slice
-#pragma unroll
-        for (int j = K - 1; j >= 0; --j)
-            if ((s[j] >> kFlagShift) == 0)
-                r = j;
-        const uint32_t full = __ballot_sync(0xffffffffu, r == K);
-        const uint32_t f = full == 0xffffffffu ? 32u : (uint32_t)__ffs(~full) - 1;
-        const uint32_t myr = lane < f ? K : (lane == f ? r : 0u);
-        const uint32_t total = __reduce_add_sync(0xffffffffu, myr);
-        if (total == 0) {
+            for (int j = 0; j < kScanPerLane; ++j)
+                if (!(have & (1u << j))) {
+                    const uint32_t t = t0 + j;
+                    s[j] = t < ntiles ? ld_acquire(&status[t]) : kFlagAgg;
+                    if (s[j] >> kFlagShift)
+                        have |= 1u << j;
+                }
+            if (__all_sync(0xffffffffu, have == (1u << kScanPerLane) - 1))
+                break;
             __nanosleep(64);
-            continue;
         }
-        uint64_t sum = 0;
+        LU_CNT(11, 1);
+        uint32_t c[kScanPerLane];
+        uint32_t lsum = 0, errj = kScanPerLane;
 #pragma unroll
-        for (int j = 0; j < K; ++j)
-            if ((uint32_t)j < myr)
-                sum = seq_combine(sum, s[j] & (kErrBit | kValMask));
-        uint64_t inc = sum;
+        for (int j = kScanPerLane - 1; j >= 0; --j) {
+            c[j] = (uint32_t)s[j]; // aggregate counts are < 2^15
+            lsum += c[j];
+            if (s[j] & kErrBit)
+                errj = (uint32_t)j;
+        }
+        uint32_t incl = lsum;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const uint64_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
             if (lane >= (uint32_t)d)
-                inc = seq_combine(o, inc);
+                incl += o;
         }
-        uint64_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
-        if (lane == 0)
-            ex = 0;
-        uint64_t run = seq_combine(acc, ex);
+        const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t errball = __ballot_sync(0xffffffffu, errj < kScanPerLane);
+        unsigned long long base = 0;
+        if (w != 0) {
+            const uint32_t slot = (w - 1) % kScanWarps;
+            if (lane == 0)
+                while (vtag[slot] != w)
+                    ;
+            __syncwarp();
+            base = vbase[slot];
+        }
+        if (lane == 0) {
+            vbase[w % kScanWarps] = (base + wtot) | (errball ? kErrBit : 0ull);
+            __threadfence_block();
+            vtag[w % kScanWarps] = w + 1;
+        }
+        const bool err_before = (base & kErrBit) || (errball & ((1u << lane) - 1u));
+        uint64_t ex = (base & kValMask) + (incl - lsum);
 #pragma unroll
-        for (int j = 0; j < K; ++j)
-            if ((uint32_t)j < myr) {
-                st_release(&status[next + lane * K + j], kFlagInc | run);
-                run = seq_combine(run, s[j] & (kErrBit | kValMask));
-            }
-        acc = seq_combine(acc, __shfl_sync(0xffffffffu, inc, 31));
-        next += total;
+        for (int j = 0; j < kScanPerLane; ++j) {
+            const uint32_t t = t0 + j;
+            if (t < ntiles)
+                st_release(&status[t], kFlagInc | ((err_before || errj < (uint32_t)j) ? kErrBit : 0ull) | ex);
+            ex += c[j];
+        }
     }
 }
 

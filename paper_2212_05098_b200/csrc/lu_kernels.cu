@@ -170,7 +170,8 @@ constexpr int kGroupWarps = 4;
 constexpr int kGroupsPerCta = 2;
 constexpr int kGroupThreads = 32 * kGroupWarps;
 constexpr int kPipeTile = kGroupWarps * kChunkBytes; // 8 KiB
-constexpr int kPipeThreads = kGroupsPerCta * kGroupThreads + 32;
+constexpr int kPipeThreads = kGroupsPerCta * kGroupThreads;
+static_assert(kPipeThreads / 32 == kScanWarps, "CTA 0's warps are the scanner warps");
 
 struct GroupShared {
     WarpResult wres[2][kGroupWarps];
@@ -228,10 +229,14 @@ __device__ __forceinline__ void pipe_resolve(GroupShared &ps, uint32_t b, uint64
 {
     const uint32_t tile = ps.tile_of[b];
     uint64_t st = ld_acquire(&status[tile]);
+    uint32_t spins = 0;
     while ((st >> kFlagShift) != 2) {
         __nanosleep(32);
         st = ld_acquire(&status[tile]);
+        ++spins;
     }
+    LU_CNT(9, spins);
+    LU_CNT(10, spins ? 1 : 0);
     const uint64_t ex = st & (kErrBit | kValMask);
     ps.excl[b] = ex;
     if (!(ex & kErrBit)) {
@@ -276,15 +281,18 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ SelPair sel[16];
     __shared__ GroupShared gshared[kGroupsPerCta];
+    __shared__ ScanShared scan_s;
 
     const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n_bytes;
     unsigned int *ticket = reinterpret_cast<unsigned int *>(status + ntiles);
     sel_table_init(sel);
+    scan_init(scan_s);
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5;
-    if (warp == kGroupsPerCta * kGroupWarps) {
-        if (blockIdx.x == 0)
-            scan_tiles<16>(status, ntiles);
+    LU_PROF_INIT();
+    if (blockIdx.x == 0) {
+        scan_windows(status, ntiles, warp, scan_s);
+        LU_PROF_FLUSH();
         return;
     }
     const uint32_t g = warp / kGroupWarps, wit = warp % kGroupWarps;
@@ -296,19 +304,30 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     uint32_t i = 0;
     for (;; ++i) {
         const uint32_t buf = i & 1;
-        // one barrier publishes both this iteration's ticket and the prefix
-        // of the tile computed two iterations ago (buffer reuse)
-        // Claim at the top: a tile is computed right after it is claimed, so
-        // the scanner never waits on a claimed-but-idle tile (claiming one
-        // tile ahead measured 15% slower).
-        if (gtid == 0) {
-            if (i >= 2)
+        // Claim after copying out the buffer being reused, right before the
+        // compute: the claim -> publish span is what the scanner frontier
+        // (and so every group's resolve) waits on, so it must hold nothing
+        // but the tile's own compute (claiming before the copy-out, or a
+        // tile ahead, measured 15-35% slower).
+        uint32_t claim = 0;
+        LU_T0();
+        if (i >= 2) {
+            if (gtid == 0)
                 pipe_resolve<Dir>(ps, buf, status, res, ntiles, lo_b, n_units);
-            ps.claim = atomicAdd(ticket, 1u);
-        }
-        bar_sync(bar_claim, kGroupThreads); // publishes ps.claim and, for i >= 2, ps.excl[buf]
-        if (i >= 2)
+            LU_T(0); // resolve (warp 0) / nothing
+            bar_sync(bar_prefix, kGroupThreads); // publishes ps.excl[buf]
+            LU_T(1); // prefix barrier wait
+            if (gtid == 0)
+                claim = atomicAdd(ticket, 1u); // in flight during the copy-out
             pipe_copy<Dir>(ps, buf, wit, out_g, out_a, out_lead);
+            LU_T(2); // copy-out
+        } else if (gtid == 0) {
+            claim = atomicAdd(ticket, 1u);
+        }
+        if (gtid == 0)
+            ps.claim = claim;
+        bar_sync(bar_claim, kGroupThreads); // publishes ps.claim
+        LU_T(3); // claim barrier wait
         const uint32_t tile = ps.claim;
         if (tile >= ntiles)
             break;
@@ -319,7 +338,10 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
             Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit);
         else
             Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit);
+        LU_T(4); // compute
         bar_sync(bar_done, kGroupThreads);
+        LU_T(5); // tile-done barrier wait
+        LU_CNT(6, 1);
         if (gtid == 0) {
             uint32_t units = 0, first = kGroupWarps;
             for (int w = 0; w < kGroupWarps; ++w) {
@@ -334,6 +356,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
             ps.tile_of[buf] = tile;
             st_release(&status[tile], kFlagAgg | (first < kGroupWarps ? kErrBit : 0ull) | (uint64_t)units);
         }
+        LU_T(7); // combine + publish
     }
     // drain the tile computed in the last iteration
     if (i >= 1) {
@@ -342,6 +365,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
         bar_sync(bar_prefix, kGroupThreads);
         pipe_copy<Dir>(ps, (i - 1) & 1, wit, out_g, out_a, out_lead);
     }
+    LU_PROF_FLUSH();
 }
 
 // ================================================================= K3 / K4
@@ -454,7 +478,8 @@ static int set_smem_attrs()
 
 // Grid of a persistent pipelined kernel: every CTA must be resident (tiles
 // wait on smaller tiles held by other CTAs), so never exceed the occupancy.
-static int persistent_grid(const void *fn, int threads, size_t smem, uint64_t ntiles, unsigned *grid)
+static int persistent_grid(const void *fn, int threads, size_t smem, uint64_t ntiles, unsigned *grid,
+                           unsigned extra = 0)
 {
     int dev = 0, sms = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -464,10 +489,11 @@ static int persistent_grid(const void *fn, int threads, size_t smem, uint64_t nt
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
     if (e != cudaSuccess)
         return cuda_fail(e, "occupancy query");
-    if (per_sm < 1)
-        return fail(LU_ERR_CUDA, "pipelined kernel cannot be resident on this device");
     const uint64_t cap = (uint64_t)sms * (uint64_t)per_sm;
-    *grid = (unsigned)(ntiles < cap ? ntiles : cap);
+    if (cap < 1 + extra)
+        return fail(LU_ERR_CUDA, "persistent kernel cannot be resident on this device");
+    // extra: CTAs that process no tiles (the transcode kernels' scanner CTA)
+    *grid = (unsigned)(ntiles + extra < cap ? ntiles + extra : cap);
     return 0;
 }
 
@@ -478,6 +504,18 @@ using namespace lu;
 extern "C" {
 
 const char *lu_last_error(void) { return g_err.c_str(); }
+
+#ifdef LU_PROF
+int lu_prof_read(unsigned long long *out32, int reset)
+{
+    cudaError_t e = cudaMemcpyFromSymbol(out32, g_prof, sizeof(g_prof));
+    if (e == cudaSuccess && reset) {
+        static const unsigned long long z[48] = {};
+        e = cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+    }
+    return e == cudaSuccess ? 0 : -1;
+}
+#endif
 
 const char *lu_version(void) { return "laneutf_b200 0.1.0 (sm_100a)"; }
 
@@ -534,7 +572,7 @@ int lu_utf8_to_utf16le(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint6
     const uint32_t out_lead = (uint32_t)(((uintptr_t)out_safe & 15) >> 1);
     uint16_t *out_a = out_safe - out_lead;
     unsigned grid = 0;
-    rc = persistent_grid((const void *)k_transcode<DirU8U16>, kPipeThreads, kSmemK1, nt, &grid);
+    rc = persistent_grid((const void *)k_transcode<DirU8U16>, kPipeThreads, kSmemK1, nt, &grid, 1);
     if (rc)
         return rc;
     k_transcode<DirU8U16><<<grid, kPipeThreads, kSmemK1, stream>>>(base, lead, n_bytes, n_bytes, out_a, out_lead,
@@ -574,7 +612,7 @@ int lu_utf16le_to_utf8(const uint16_t *in, uint64_t n_words, uint8_t *out, uint6
     uint8_t *out_safe = out ? out : reinterpret_cast<uint8_t *>(16);
     const uint32_t out_lead = (uint32_t)((uintptr_t)out_safe & 15);
     unsigned grid = 0;
-    rc = persistent_grid((const void *)k_transcode<DirU16U8>, kPipeThreads, kSmemK2, nt, &grid);
+    rc = persistent_grid((const void *)k_transcode<DirU16U8>, kPipeThreads, kSmemK2, nt, &grid, 1);
     if (rc)
         return rc;
     k_transcode<DirU16U8><<<grid, kPipeThreads, kSmemK2, stream>>>(
