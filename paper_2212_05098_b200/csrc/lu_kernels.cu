@@ -192,11 +192,18 @@ struct DirU8U16 {
     using OutT = uint16_t;
     static constexpr int kStride = kOutStrideU16;
     static constexpr int kUnitShift = 0; // input positions are bytes
+    using In = ChunkIn;
+    template <bool B>
+    __device__ static void load(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, uint32_t wit,
+                                In &in)
+    {
+        load_chunk<B>(base, tile_off + (int64_t)wit * kChunkBytes, lo_b, hi_b, in);
+    }
     template <bool B>
     __device__ static void compute(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, OutT *out_w,
-                                   const SelPair *sel, WarpResult &wr, uint32_t wit)
+                                   const SelPair *sel, WarpResult &wr, uint32_t wit, const In &in)
     {
-        u8u16_warp<B>(base, tile_off, lo_b, hi_b, out_w, sel, wr, wit);
+        u8u16_warp<B>(base, tile_off, lo_b, hi_b, out_w, sel, wr, wit, in);
     }
     __device__ static void copy_out(const OutT *src, uint32_t cnt, OutT *out_a, uint64_t g0)
     {
@@ -208,9 +215,14 @@ struct DirU16U8 {
     using OutT = uint8_t;
     static constexpr int kStride = kOutStrideU8;
     static constexpr int kUnitShift = 1; // input positions are 16-bit words
+    struct In {};
+    template <bool B>
+    __device__ static void load(const uint8_t *, int64_t, int64_t, int64_t, uint32_t, In &)
+    {
+    }
     template <bool B>
     __device__ static void compute(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, OutT *out_w,
-                                   const SelPair *, WarpResult &wr, uint32_t wit)
+                                   const SelPair *, WarpResult &wr, uint32_t wit, const In &)
     {
         u16u8_warp_r<B>(base, tile_off, lo_b, hi_b, out_w, wr, wit);
     }
@@ -225,10 +237,11 @@ struct DirU16U8 {
 // the last tile.
 template <class Dir>
 __device__ __forceinline__ void pipe_resolve(GroupShared &ps, uint32_t b, uint64_t *status, Outcome *res,
-                                             uint32_t ntiles, int64_t lo_b, uint64_t n_units)
+                                             uint32_t ntiles, int64_t lo_b, uint64_t n_units, uint64_t st)
 {
     const uint32_t tile = ps.tile_of[b];
-    uint64_t st = ld_acquire(&status[tile]);
+    if ((st >> kFlagShift) != 2)
+        st = ld_acquire(&status[tile]);
     uint32_t spins = 0;
     while ((st >> kFlagShift) != 2) {
         __nanosleep(32);
@@ -302,43 +315,48 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     OutT *out_g = reinterpret_cast<OutT *>(smem_raw) + g * (2 * kGroupWarps * Dir::kStride);
 
     uint32_t i = 0;
+    uint64_t st_pre = 0; // group thread 0: early poll of the next status word to resolve
     for (;; ++i) {
         const uint32_t buf = i & 1;
-        // Claim after copying out the buffer being reused, right before the
-        // compute: the claim -> publish span is what the scanner frontier
-        // (and so every group's resolve) waits on, so it must hold nothing
-        // but the tile's own compute (claiming before the copy-out, or a
-        // tile ahead, measured 15-35% slower).
-        uint32_t claim = 0;
+        // Group thread 0 claims the next tile (atomic in flight) and resolves
+        // the buffer about to be reused; one barrier publishes both.  The
+        // tile's input loads are then issued before the copy-out of that
+        // buffer, so the copy-out hides their latency.
         LU_T0();
-        if (i >= 2) {
-            if (gtid == 0)
-                pipe_resolve<Dir>(ps, buf, status, res, ntiles, lo_b, n_units);
-            LU_T(0); // resolve (warp 0) / nothing
-            bar_sync(bar_prefix, kGroupThreads); // publishes ps.excl[buf]
-            LU_T(1); // prefix barrier wait
-            if (gtid == 0)
-                claim = atomicAdd(ticket, 1u); // in flight during the copy-out
-            pipe_copy<Dir>(ps, buf, wit, out_g, out_a, out_lead);
-            LU_T(2); // copy-out
-        } else if (gtid == 0) {
-            claim = atomicAdd(ticket, 1u);
-        }
-        if (gtid == 0)
+        if (gtid == 0) {
+            const uint32_t claim = atomicAdd(ticket, 1u);
+            if (i >= 2)
+                pipe_resolve<Dir>(ps, buf, status, res, ntiles, lo_b, n_units, st_pre);
             ps.claim = claim;
-        bar_sync(bar_claim, kGroupThreads); // publishes ps.claim
+        }
+        LU_T(0); // claim + resolve (warp 0) / nothing
+        bar_sync(bar_claim, kGroupThreads); // publishes ps.claim and, for i >= 2, ps.excl[buf]
         LU_T(3); // claim barrier wait
         const uint32_t tile = ps.claim;
+        const int64_t tile_off = (int64_t)tile * kPipeTile;
+        const bool interior = (tile_off - 4 >= lo_b) && (tile_off + kPipeTile + 4 <= hi_b);
+        typename Dir::In in;
+        if (tile < ntiles) {
+            if (interior)
+                Dir::template load<false>(base, tile_off, lo_b, hi_b, wit, in);
+            else
+                Dir::template load<true>(base, tile_off, lo_b, hi_b, wit, in);
+        }
+        if (i >= 2)
+            pipe_copy<Dir>(ps, buf, wit, out_g, out_a, out_lead);
+        LU_T(2); // copy-out
         if (tile >= ntiles)
             break;
-        const int64_t tile_off = (int64_t)tile * kPipeTile;
         OutT *out_w = out_g + (buf * kGroupWarps + wit) * Dir::kStride;
-        const bool interior = (tile_off - 4 >= lo_b) && (tile_off + kPipeTile + 4 <= hi_b);
         if (interior)
-            Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit);
+            Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in);
         else
-            Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit);
+            Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in);
         LU_T(4); // compute
+        // poll the status word resolved at the top of the next iteration now:
+        // its L2 round trip overlaps the other warps' compute
+        if (gtid == 0 && i >= 1)
+            st_pre = ld_acquire(&status[ps.tile_of[buf ^ 1]]);
         bar_sync(bar_done, kGroupThreads);
         LU_T(5); // tile-done barrier wait
         LU_CNT(6, 1);
@@ -361,7 +379,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     // drain the tile computed in the last iteration
     if (i >= 1) {
         if (gtid == 0)
-            pipe_resolve<Dir>(ps, (i - 1) & 1, status, res, ntiles, lo_b, n_units);
+            pipe_resolve<Dir>(ps, (i - 1) & 1, status, res, ntiles, lo_b, n_units, 0);
         bar_sync(bar_prefix, kGroupThreads);
         pipe_copy<Dir>(ps, (i - 1) & 1, wit, out_g, out_a, out_lead);
     }

@@ -316,20 +316,38 @@ __device__ __forceinline__ void sts16_if(uint32_t addr, uint32_t v, uint32_t roo
                  : "memory");
 }
 
+// A warp's 2 KiB input chunk in registers (16 B per lane per round) plus the
+// 4-byte halos; loaded separately so a caller can issue the loads early and
+// overlap their latency with other work (the pipelined copy-out).
+struct ChunkIn {
+    uint4 q[kChunkBytes / 512];
+    uint32_t halo_p; // lane 0: the 4 bytes before the chunk
+    uint32_t halo_n; // lane 31: the 4 bytes after it
+};
+
+template <bool Boundary>
+__device__ __forceinline__ void load_chunk(const uint8_t *__restrict__ base, int64_t chunk, int64_t lo_b, int64_t hi_b,
+                                           ChunkIn &in)
+{
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (int r = 0; r < kChunkBytes / 512; ++r)
+        in.q[r] = ld16(base, chunk + r * 512 + 16 * (int64_t)lane, lo_b, hi_b, Boundary);
+    in.halo_p = (lane == 0) ? halo4<Boundary>(base, chunk - 4, lo_b, hi_b) : 0u;
+    in.halo_n = (lane == 31) ? halo4<Boundary>(base, chunk + kChunkBytes, lo_b, hi_b) : 0u;
+}
+
 template <bool Boundary>
 __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
                                            int64_t hi_b, uint16_t *out_w, const SelPair *sel, WarpResult &wr,
-                                           uint32_t warp /* warp index inside the tile */)
+                                           uint32_t warp /* warp index inside the tile */, const ChunkIn &in)
 {
     const uint32_t lane = lane_id();
     const int64_t chunk = tile_off + (int64_t)warp * kChunkBytes;
     constexpr int kRounds = kChunkBytes / 512;
-    uint4 q[kRounds];
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r)
-        q[r] = ld16(base, chunk + r * 512 + 16 * (int64_t)lane, lo_b, hi_b, Boundary);
-    uint32_t carry = (lane == 0) ? halo4<Boundary>(base, chunk - 4, lo_b, hi_b) : 0u;
-    const uint32_t halo_n = (lane == 31) ? halo4<Boundary>(base, chunk + kChunkBytes, lo_b, hi_b) : 0u;
+    const uint4 *q = in.q;
+    uint32_t carry = in.halo_p;
+    const uint32_t halo_n = in.halo_n;
     uint32_t rn[kRounds];
 #pragma unroll
     for (int r = 0; r < kRounds; ++r)

@@ -1,5 +1,5 @@
 """Summarise an ncu report's source page: instructions per 128-byte step by
-source line and SASS opcode.  usage: python tools/ncu_lines.py REPORT [MiB] [top]"""
+source line and SASS opcode.  usage: python tools/ncu_lines.py REPORT [MiB] [top] [launch-index]"""
 import collections
 import csv
 import subprocess
@@ -8,7 +8,9 @@ import sys
 rep = sys.argv[1]
 mib = float(sys.argv[2]) if len(sys.argv) > 2 else 256
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+launch = sys.argv[4] if len(sys.argv) > 4 else None  # one launch of the report (default: all merged)
+extra = ["--launch-skip", launch, "--launch-count", "1"] if launch is not None else []
+txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + extra,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(txt.splitlines()))
 cur = None
