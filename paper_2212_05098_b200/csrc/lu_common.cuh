@@ -262,6 +262,56 @@ __device__ __forceinline__ uint4 load_u128_masked(const uint8_t *base, int64_t a
     return v;
 }
 
+// ------------------------------------------------------ warp chunk loads
+
+__device__ __forceinline__ uint4 ld16(const uint8_t *base, int64_t a, int64_t lo, int64_t hi, bool boundary)
+{
+    if (!boundary)
+        return __ldcs(reinterpret_cast<const uint4 *>(base + a));
+    if (a + 16 <= lo || a >= hi)
+        return make_uint4(0, 0, 0, 0);
+    return load_u128_masked(base, a, lo, hi);
+}
+
+__device__ __forceinline__ uint32_t ld4(const uint8_t *base, int64_t a, int64_t lo, int64_t hi)
+{
+    if (a + 4 <= lo || a >= hi)
+        return 0u;
+    if (a >= lo && a + 4 <= hi)
+        return __ldg(reinterpret_cast<const uint32_t *>(base + a));
+    return load_u32_masked(base, a, lo, hi);
+}
+
+// 4-byte halo word; interior tiles are known to be in bounds
+template <bool Boundary>
+__device__ __forceinline__ uint32_t halo4(const uint8_t *base, int64_t a, int64_t lo, int64_t hi)
+{
+    if (!Boundary)
+        return __ldg(reinterpret_cast<const uint32_t *>(base + a));
+    return ld4(base, a, lo, hi);
+}
+
+// A warp's 2 KiB input chunk in registers (16 B per lane per round) plus the
+// 4-byte halos; loaded separately so a caller can issue the loads early and
+// overlap their latency with other work (the pipelined copy-out).
+struct ChunkIn {
+    uint4 q[kChunkBytes / 512];
+    uint32_t halo_p; // lane 0: the 4 bytes before the chunk
+    uint32_t halo_n; // lane 31: the 4 bytes after it
+};
+
+template <bool Boundary>
+__device__ __forceinline__ void load_chunk(const uint8_t *__restrict__ base, int64_t chunk, int64_t lo_b, int64_t hi_b,
+                                           ChunkIn &in)
+{
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (int r = 0; r < kChunkBytes / 512; ++r)
+        in.q[r] = ld16(base, chunk + r * 512 + 16 * (int64_t)lane, lo_b, hi_b, Boundary);
+    in.halo_p = (lane == 0) ? halo4<Boundary>(base, chunk - 4, lo_b, hi_b) : 0u;
+    in.halo_n = (lane == 31) ? halo4<Boundary>(base, chunk + kChunkBytes, lo_b, hi_b) : 0u;
+}
+
 // Per-quad validity mask (bit 7 of each byte whose logical position is in
 // [0, n)) for boundary tiles.
 __device__ __forceinline__ uint32_t valid_mask(int64_t a, int64_t lo, int64_t hi)

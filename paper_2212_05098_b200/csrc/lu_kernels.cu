@@ -215,16 +215,18 @@ struct DirU16U8 {
     using OutT = uint8_t;
     static constexpr int kStride = kOutStrideU8;
     static constexpr int kUnitShift = 1; // input positions are 16-bit words
-    struct In {};
+    using In = ChunkIn;
     template <bool B>
-    __device__ static void load(const uint8_t *, int64_t, int64_t, int64_t, uint32_t, In &)
+    __device__ static void load(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, uint32_t wit,
+                                In &in)
     {
+        load_chunk<B>(base, tile_off + (int64_t)wit * kChunkBytes, lo_b, hi_b, in);
     }
     template <bool B>
     __device__ static void compute(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, OutT *out_w,
-                                   const SelPair *, WarpResult &wr, uint32_t wit, const In &)
+                                   const SelPair *, WarpResult &wr, uint32_t wit, const In &in)
     {
-        u16u8_warp_r<B>(base, tile_off, lo_b, hi_b, out_w, wr, wit);
+        u16u8_warp_r<B>(base, tile_off, lo_b, hi_b, out_w, wr, wit, in);
     }
     __device__ static void copy_out(const OutT *src, uint32_t cnt, OutT *out_a, uint64_t g0)
     {

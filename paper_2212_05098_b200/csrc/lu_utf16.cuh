@@ -79,33 +79,15 @@ __device__ __forceinline__ void sts8_if(uint32_t addr, uint32_t v, uint32_t n, u
 // fast path skips the surrogate logic when a round has no surrogate.
 template <bool Boundary>
 __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
-                                             int64_t hi_b, uint8_t *out_w, WarpResult &wr, uint32_t warp)
+                                             int64_t hi_b, uint8_t *out_w, WarpResult &wr, uint32_t warp,
+                                             const ChunkIn &in)
 {
     const uint32_t lane = lane_id();
     const int64_t chunk = tile_off + (int64_t)warp * kChunkBytes;
     constexpr int kRounds = kChunkBytes / 512;
-    uint4 q[kRounds];
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
-        const int64_t a = chunk + r * 512 + 16 * (int64_t)lane;
-        if (!Boundary)
-            q[r] = __ldcs(reinterpret_cast<const uint4 *>(base + a));
-        else if (a + 16 <= lo_b || a >= hi_b)
-            q[r] = make_uint4(0, 0, 0, 0);
-        else
-            q[r] = load_u128_masked(base, a, lo_b, hi_b);
-    }
-    uint32_t carry = 0, halo_n = 0;
-    if (lane == 0) {
-        const int64_t a = chunk - 4;
-        carry = Boundary ? ((a + 4 <= lo_b || a >= hi_b) ? 0u : load_u32_masked(base, a, lo_b, hi_b))
-                         : __ldg(reinterpret_cast<const uint32_t *>(base + a));
-    }
-    if (lane == 31) {
-        const int64_t a = chunk + kChunkBytes;
-        halo_n = Boundary ? ((a + 4 <= lo_b || a >= hi_b) ? 0u : load_u32_masked(base, a, lo_b, hi_b))
-                          : __ldg(reinterpret_cast<const uint32_t *>(base + a));
-    }
+    const uint4 *q = in.q;
+    uint32_t carry = in.halo_p;
+    const uint32_t halo_n = in.halo_n;
     uint32_t rn[kRounds];
 #pragma unroll
     for (int r = 0; r < kRounds; ++r)
