@@ -318,6 +318,11 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
 
     uint32_t i = 0;
     uint64_t st_pre = 0; // group thread 0: early poll of the next status word to resolve
+    // group thread 0: the next tile; the ticket is taken right after the
+    // tile-done barrier so its latency overlaps the combine + publish
+    uint32_t next_claim = 0;
+    if (gtid == 0)
+        next_claim = atomicAdd(ticket, 1u);
     for (;; ++i) {
         const uint32_t buf = i & 1;
         // Group thread 0 claims the next tile (atomic in flight) and resolves
@@ -326,10 +331,9 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
         // buffer, so the copy-out hides their latency.
         LU_T0();
         if (gtid == 0) {
-            const uint32_t claim = atomicAdd(ticket, 1u);
             if (i >= 2)
                 pipe_resolve<Dir>(ps, buf, status, res, ntiles, lo_b, n_units, st_pre);
-            ps.claim = claim;
+            ps.claim = next_claim;
         }
         LU_T(0); // claim + resolve (warp 0) / nothing
         bar_sync(bar_claim, kGroupThreads); // publishes ps.claim and, for i >= 2, ps.excl[buf]
@@ -363,6 +367,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
         LU_T(5); // tile-done barrier wait
         LU_CNT(6, 1);
         if (gtid == 0) {
+            next_claim = atomicAdd(ticket, 1u);
             uint32_t units = 0, first = kGroupWarps;
             for (int w = 0; w < kGroupWarps; ++w) {
                 ps.warp_excl[buf][w] = units;
