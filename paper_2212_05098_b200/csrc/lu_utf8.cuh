@@ -122,6 +122,8 @@ struct WarpResult {
 //   path 0  no byte >= E0 in the round or its look-behind: ASCII + 2-byte
 //           leads only, "must be continuation" = L(i-1);
 //   path 1  no F-class byte and no 2-byte lead: ASCII + 3-byte leads;
+//   path 3  no 2-byte and no 3-byte lead: ASCII + 4-byte leads (text
+//           outside the BMP, e.g. emoji); only the F0/F4/F5+ range check;
 //   path 2  everything else (general detector and decoder).
 // Every path flags every bad byte its class mix can contain.
 struct U8Round {
@@ -175,13 +177,15 @@ __device__ __forceinline__ void u8_round_detect(U8Round &R)
         R.det = det;
         return;
     }
-    uint32_t anyf = 0, any2 = 0;
+    uint32_t anyf = 0, any2 = 0, any3 = 0;
 #pragma unroll
     for (int k = 0; k <= 4; ++k) {
         R.m[k].F = R.m[k].E & (R.w[k] << 3);
         anyf |= R.m[k].F;
-        if (k > 0)
+        if (k > 0) {
             any2 |= R.m[k].L & ~R.m[k].E;
+            any3 |= R.m[k].E & ~R.m[k].F;
+        }
     }
     if (!__any_sync(0xffffffffu, (anyf | any2) != 0)) {
         R.path = 1;
@@ -196,6 +200,17 @@ __device__ __forceinline__ void u8_round_detect(U8Round &R)
 #pragma unroll
             for (int k = 1; k <= 4; ++k)
                 det |= u8_check_e(R.w[k], fsr(R.w[k], R.w[k + 1], 8), R.m[k]);
+        }
+        R.det = det;
+        return;
+    }
+    if (!__any_sync(0xffffffffu, (any2 | any3) != 0)) {
+        R.path = 3;
+#pragma unroll
+        for (int k = 1; k <= 4; ++k) {
+            const U8Masks &c = R.m[k], &p = R.m[k - 1];
+            det |= (fsl(p.L, c.L, 8) | fsl(p.E, c.E, 16) | fsl(p.F, c.F, 24)) ^ c.C;
+            det |= u8_check_f(R.w[k], fsr(R.w[k], R.w[k + 1], 8), c);
         }
         R.det = det;
         return;
@@ -254,6 +269,26 @@ __device__ __forceinline__ void u8_decode_quad(uint32_t x, uint32_t xn, const U8
         lo |= (lo4 & sF) | (lo3 & sS);
         hi |= (hi4 & sF) | (hiS & sS);
     }
+}
+
+// path 3: ASCII and 4-byte leads only.  Non-ASCII bytes are F leads (high
+// surrogate) or continuations; every continuation gets the low-surrogate
+// form, which is right for the first one after a lead and never emitted for
+// the others.
+__device__ __forceinline__ void u8_decode4(uint32_t x, uint32_t xn, const U8Masks &m, uint32_t &lo, uint32_t &hi)
+{
+    const uint32_t n1 = fsr(x, xn, 8);
+    const uint32_t n2 = fsr(x, xn, 16);
+    const uint32_t lo3 = ((n1 << 6) & 0xC0C0C0C0u) | (n2 & 0x3F3F3F3Fu);
+    const uint32_t mm = ((n1 << 2) & 0xFCFCFCFCu) | ((n2 >> 4) & 0x03030303u);
+    const uint32_t lo4 = ((mm | H8) - 0x40404040u) ^ (~mm & H8); // bytewise mm - 0x40
+    const uint32_t carry = ((n1 >> 4) | (n1 >> 5)) & 0x01010101u;
+    const uint32_t hi4 = (x & 0x07070707u) + carry + 0xD7D7D7D7u;
+    const uint32_t hiS = 0xDCDCDCDCu | ((n1 >> 2) & 0x03030303u);
+    const uint32_t sA = sgn8(x);
+    const uint32_t sF = sgn8(m.F);
+    lo = (x & ~sA) | (((lo4 & sF) | (lo3 & ~sF)) & sA);
+    hi = ((hi4 & sF) | (hiS & ~sF)) & sA;
 }
 
 // path 0: ASCII and 2-byte leads only
@@ -330,7 +365,7 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
         uint32_t e[4], fi1[4], c[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            if (R.path == 2) {
+            if (R.path >= 2) {
                 fi1[k] = fsl(R.m[k].F, R.m[k + 1].F, 8);
                 e[k] = (~R.m[k + 1].C | fi1[k]) & H8;
             } else {
@@ -427,6 +462,10 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 u8_decode3(R.w[k + 1], R.w[k + 2], lop[k], hip[k]);
+        } else if (R.path == 3) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                u8_decode4(R.w[k + 1], R.w[k + 2], R.m[k + 1], lop[k], hip[k]);
         } else {
 #pragma unroll
             for (int k = 0; k < 4; ++k)

@@ -136,8 +136,9 @@ def _boundary_positions(n):
     return sorted(pos)
 
 
-def test_utf8_errors_at_boundaries(cuda_ok):
-    base = corpus.generate("mix", 3 * TILE + 777, seed=21).numpy()
+@pytest.mark.parametrize("profile", ["mix", "latin", "cjk", "emoji"])  # detector paths 2, 0, 1, 3
+def test_utf8_errors_at_boundaries(cuda_ok, profile):
+    base = corpus.generate(profile, 3 * TILE + 777, seed=21).numpy()
     rng = random.Random(7)
     patterns = [b"\x80", b"\xc0", b"\xc1\xbf", b"\xe0\x80\x80", b"\xed\xa0\x80", b"\xf0\x8f\xbf\xbf",
                 b"\xf4\x90\x80\x80", b"\xf5", b"\xff", b"\xe2\x28", b"\xc2", b"\xf0\x9f\x98"]
@@ -300,9 +301,10 @@ def test_config4_error_injection(cuda_ok, utf16):
         assert out[: got.written].cpu().numpy().tobytes() == ref_out[: got.written].tobytes()
 
 
+@pytest.mark.parametrize("profile", ["latin", "cyrillic", "cjk", "emoji"])
 @pytest.mark.parametrize("kind", corpus.UTF8_ERROR_KINDS)
-def test_each_utf8_error_kind(cuda_ok, kind):
-    base = corpus.generate("cjk", 200_000, seed=9).numpy()
+def test_each_utf8_error_kind(cuda_ok, kind, profile):
+    base = corpus.generate(profile, 200_000, seed=9).numpy()
     for s in range(20):
         data = torch.from_numpy(base.copy())
         corpus.inject_errors(data, utf16=False, rate=2e-5, seed=500 + s, kinds=(kind,))
