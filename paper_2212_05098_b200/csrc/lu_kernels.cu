@@ -179,6 +179,7 @@ struct GroupShared {
     uint64_t excl[2];
     uint32_t first_err[2];
     uint32_t tile_of[2];
+    uint32_t units[2]; // tile output units before its first error (or all)
     uint32_t claim;
 };
 
@@ -256,10 +257,7 @@ __device__ __forceinline__ void pipe_resolve(GroupShared &ps, uint32_t b, uint64
     ps.excl[b] = ex;
     if (!(ex & kErrBit)) {
         const uint32_t first = ps.first_err[b];
-        uint64_t units = 0;
-        for (uint32_t w = 0; w < kGroupWarps && w <= first; ++w)
-            units += ps.wres[b][w].units;
-        const uint64_t written = ex + units;
+        const uint64_t written = ex + ps.units[b];
         const int64_t tile_off = (int64_t)tile * kPipeTile;
         if (first < kGroupWarps) {
             res->status = kStatusMalformed;
@@ -333,7 +331,9 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
         if (gtid == 0) {
             if (i >= 2)
                 pipe_resolve<Dir>(ps, buf, status, res, ntiles, lo_b, n_units, st_pre);
+            LU_T(12); // resolve
             ps.claim = next_claim;
+            LU_T(13); // ticket wait
         }
         LU_T(0); // claim + resolve (warp 0) / nothing
         bar_sync(bar_claim, kGroupThreads); // publishes ps.claim and, for i >= 2, ps.excl[buf]
@@ -366,20 +366,32 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
         bar_sync(bar_done, kGroupThreads);
         LU_T(5); // tile-done barrier wait
         LU_CNT(6, 1);
-        if (gtid == 0) {
-            next_claim = atomicAdd(ticket, 1u);
-            uint32_t units = 0, first = kGroupWarps;
-            for (int w = 0; w < kGroupWarps; ++w) {
-                ps.warp_excl[buf][w] = units;
-                units += ps.wres[buf][w].units;
-                if (ps.wres[buf][w].err) {
-                    first = (uint32_t)w;
-                    break;
-                }
+        if (wit == 0) {
+            // combine the 4 warp results on lanes 0..3 (shallow dependency
+            // chain: this is on the group's critical path)
+            const uint32_t lane = gtid;
+            if (lane == 0)
+                next_claim = atomicAdd(ticket, 1u);
+            const WarpResult r = ps.wres[buf][lane & (kGroupWarps - 1)];
+            const uint32_t errm = __ballot_sync(0xffffffffu, lane < kGroupWarps && r.err);
+            const uint32_t first = errm ? (uint32_t)__ffs(errm) - 1 : kGroupWarps;
+            const uint32_t u = (lane < kGroupWarps && lane <= first) ? r.units : 0u;
+            uint32_t inc = u;
+            uint32_t o = __shfl_up_sync(0xffffffffu, inc, 1);
+            if (lane >= 1)
+                inc += o;
+            o = __shfl_up_sync(0xffffffffu, inc, 2);
+            if (lane >= 2)
+                inc += o;
+            if (lane < kGroupWarps)
+                ps.warp_excl[buf][lane] = inc - u;
+            const uint32_t units = __shfl_sync(0xffffffffu, inc, kGroupWarps - 1);
+            if (lane == 0) {
+                ps.first_err[buf] = first;
+                ps.tile_of[buf] = tile;
+                ps.units[buf] = units;
+                st_release(&status[tile], kFlagAgg | (first < kGroupWarps ? kErrBit : 0ull) | (uint64_t)units);
             }
-            ps.first_err[buf] = first;
-            ps.tile_of[buf] = tile;
-            st_release(&status[tile], kFlagAgg | (first < kGroupWarps ? kErrBit : 0ull) | (uint64_t)units);
         }
         LU_T(7); // combine + publish
     }

@@ -57,6 +57,7 @@ def main():
                      f"{100 * w0[13] / max(w0[11], 1):.1f}% empty, {100 * w0[14] / max(w0[11], 1):.1f}% full, "
                      f"cycles/pass: issue {w0[16] / max(w0[11], 1):.0f} load-wait {w0[17] / max(w0[11], 1):.0f} "
                      f"process {w0[18] / max(w0[11] - w0[13], 1):.0f} (per non-empty pass) empty {w0[19] / max(w0[13], 1):.0f}")
+            line += f"\n   warp0 split: resolve {w0[12] / max(w0[6], 1):.0f}  ticket wait {w0[13] / max(w0[6], 1):.0f}"
             line += f"\n   resolves that spun {100 * w0[10] / max(w0[6], 1):.1f}%, {w0[9] / max(w0[10], 1):.1f} spins each"
             print(line)
 
