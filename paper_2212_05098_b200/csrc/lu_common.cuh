@@ -134,14 +134,23 @@ __shared__ unsigned long long s_prof[10][24]; // [warp][counter], lane 0 only
 
 // Central scanner: the kScanWarps warps of CTA 0 (which computes no tiles).
 // Tiles publish only their aggregate (flag 1).  Scanner warp k owns the
-// fixed windows k, k + kScanWarps, ... of kScanWindow tiles: it polls until
-// every tile of its window has published, scans the window locally (lane l
-// holds tiles [4l, 4l+4)), takes the window base from the previous window's
-// warp through shared memory, hands on its own end value, and replaces each
-// entry by flag 2 | EXCLUSIVE prefix.  Only the base hand-off is serial; the
-// polling, local scans and stores of kScanWarps windows proceed in parallel
-// (one warp sweeping serially was the throughput limit: ~3 us per pass).
-// A tile's owner just polls its own status word.
+// fixed windows k, k + kScanWarps, ... of kScanWindow tiles (lane l holds
+// tiles [4l, 4l+4) of a window).  It takes the window base from the previous
+// window's warp through shared memory, then repeatedly polls the window and
+// replaces every newly published entry of the window's leading published run
+// by flag 2 | EXCLUSIVE prefix; once the whole window is done it hands its end
+// value on.  Only the base hand-off is serial; kScanWarps windows are polled
+// and scanned in parallel (one warp sweeping serially was the throughput
+// limit: ~3 us per pass).  A tile's owner just polls its own status word.
+//
+// A window is normally published in one shot once all its tiles are in.
+// Progress: a group may hold a claimed, unpublished tile while it waits for
+// the prefix of an older tile in the same window, so waiting for the whole
+// window could deadlock.  If a window stays incomplete kPartialAfter cycles
+// after its first tile was published, its leading published run is published
+// on every poll from then on; a tile's prefix then depends only on tiles
+// before it, which guarantees progress.  (Publishing the run on every poll
+// from the start is correct too but cost K1 ~50%: scanner throughput.)
 //
 // Errors: the count of a tile at or after the first malformed tile is never
 // used (nothing there is copied out), so a prefix is the plain sum of the
@@ -150,6 +159,7 @@ __shared__ unsigned long long s_prof[10][24]; // [warp][counter], lane 0 only
 constexpr int kScanWarps = 8;
 constexpr int kScanPerLane = 4;
 constexpr uint32_t kScanWindow = 32 * kScanPerLane; // 128 tiles
+constexpr long long kPartialAfter = 40000;           // SM cycles (~20 us)
 
 struct ScanShared {
     unsigned long long base[kScanWarps]; // end value of the window in the slot
@@ -170,8 +180,13 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
     volatile uint32_t *vtag = ss.tag;
     for (uint32_t w = sw; w < nwin; w += kScanWarps) {
         const uint32_t t0 = w * kScanWindow + lane * kScanPerLane;
+        unsigned long long base = 0;
+        bool have_base = w == 0; // the base is taken only when first needed
         uint64_t s[kScanPerLane];
         uint32_t have = 0; // bit j: s[j] holds a published aggregate
+        uint32_t done = 0; // entries of the window already replaced by prefixes
+        long long t_first = 0; // clock when the first tile of the window was seen
+        bool partial = false;
         for (;;) {
 #pragma unroll
             for (int j = 0; j < kScanPerLane; ++j)
@@ -181,51 +196,71 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                     if (s[j] >> kFlagShift)
                         have |= 1u << j;
                 }
-            if (__all_sync(0xffffffffu, have == (1u << kScanPerLane) - 1))
-                break;
+            // leading published run of the window: lanes before the first
+            // lane with a gap are full; that lane contributes its own run
+            const uint32_t lrun = (uint32_t)__ffs(~have) - 1; // 0..4 (have < 16)
+            const uint32_t notfull = __ballot_sync(0xffffffffu, lrun < kScanPerLane);
+            const uint32_t fl = notfull ? (uint32_t)__ffs(notfull) - 1 : 32u;
+            const uint32_t myr = lane < fl ? kScanPerLane : (lane == fl ? lrun : 0u);
+            const uint32_t run = kScanPerLane * fl + (fl < 32 ? __shfl_sync(0xffffffffu, lrun, fl & 31) : 0u);
+            if (!partial && run != kScanWindow) {
+                if (__any_sync(0xffffffffu, have != 0)) {
+                    const long long now = clock64();
+                    if (t_first == 0)
+                        t_first = now;
+                    partial = now - t_first > kPartialAfter;
+                }
+                partial = __shfl_sync(0xffffffffu, partial, 0);
+            }
+            if (run > done && (partial || run == kScanWindow)) {
+                LU_CNT(11, 1);
+                if (!have_base) {
+                    const uint32_t slot = (w - 1) % kScanWarps;
+                    if (lane == 0)
+                        while (vtag[slot] != w)
+                            ;
+                    __syncwarp();
+                    base = vbase[slot];
+                    have_base = true;
+                }
+                uint32_t lsum = 0, errj = kScanPerLane;
+#pragma unroll
+                for (int j = kScanPerLane - 1; j >= 0; --j)
+                    if ((uint32_t)j < myr) {
+                        lsum += (uint32_t)s[j]; // aggregate counts are < 2^15
+                        if (s[j] & kErrBit)
+                            errj = (uint32_t)j;
+                    }
+                uint32_t incl = lsum;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= (uint32_t)d)
+                        incl += o;
+                }
+                const uint32_t errball = __ballot_sync(0xffffffffu, errj < kScanPerLane);
+                const bool err_before = (base & kErrBit) || (errball & ((1u << lane) - 1u));
+                uint64_t ex = (base & kValMask) + (incl - lsum);
+#pragma unroll
+                for (int j = 0; j < kScanPerLane; ++j) {
+                    const uint32_t idx = lane * kScanPerLane + j;
+                    if ((uint32_t)j < myr && idx >= done && t0 + j < ntiles)
+                        st_release(&status[t0 + j],
+                                   kFlagInc | ((err_before || errj < (uint32_t)j) ? kErrBit : 0ull) | ex);
+                    ex += (uint32_t)s[j];
+                }
+                done = run;
+                if (run == kScanWindow) {
+                    const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+                    if (lane == 0) {
+                        vbase[w % kScanWarps] = (base + wtot) | (errball ? kErrBit : 0ull);
+                        __threadfence_block();
+                        vtag[w % kScanWarps] = w + 1;
+                    }
+                    break;
+                }
+            }
             __nanosleep(64);
-        }
-        LU_CNT(11, 1);
-        uint32_t c[kScanPerLane];
-        uint32_t lsum = 0, errj = kScanPerLane;
-#pragma unroll
-        for (int j = kScanPerLane - 1; j >= 0; --j) {
-            c[j] = (uint32_t)s[j]; // aggregate counts are < 2^15
-            lsum += c[j];
-            if (s[j] & kErrBit)
-                errj = (uint32_t)j;
-        }
-        uint32_t incl = lsum;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= (uint32_t)d)
-                incl += o;
-        }
-        const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
-        const uint32_t errball = __ballot_sync(0xffffffffu, errj < kScanPerLane);
-        unsigned long long base = 0;
-        if (w != 0) {
-            const uint32_t slot = (w - 1) % kScanWarps;
-            if (lane == 0)
-                while (vtag[slot] != w)
-                    ;
-            __syncwarp();
-            base = vbase[slot];
-        }
-        if (lane == 0) {
-            vbase[w % kScanWarps] = (base + wtot) | (errball ? kErrBit : 0ull);
-            __threadfence_block();
-            vtag[w % kScanWarps] = w + 1;
-        }
-        const bool err_before = (base & kErrBit) || (errball & ((1u << lane) - 1u));
-        uint64_t ex = (base & kValMask) + (incl - lsum);
-#pragma unroll
-        for (int j = 0; j < kScanPerLane; ++j) {
-            const uint32_t t = t0 + j;
-            if (t < ntiles)
-                st_release(&status[t], kFlagInc | ((err_before || errj < (uint32_t)j) ? kErrBit : 0ull) | ex);
-            ex += c[j];
         }
     }
 }

@@ -359,3 +359,42 @@ def test_facade_routes_pinned_host_buffers(cuda_ok):
     ref, payload = oracle.utf8_to_utf16le(data.numpy())
     assert got.as_tuple() == ref
     assert out[: len(payload)].numpy().tobytes() == payload
+
+
+# ------------------------------------------------ scanner progress (no deadlock)
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("utf16", [False, True])
+def test_kernels_on_pinned_host_buffers(cuda_ok, utf16):
+    """The kernels read/write pinned host memory directly (zero-copy PCIe).
+    Slow, uneven tile loads made a group wait on a window holding its own
+    claimed tile; the scanner's partial-window fallback must keep progressing
+    (this hung before it).  Results must equal the device-memory run."""
+    from paper_2212_05098_b200 import _native
+
+    dev = torch.device("cuda", 0)
+    op = _native.OP_UTF16LE_TO_UTF8 if utf16 else _native.OP_UTF8_TO_UTF16LE
+    for profile, seed in (("latin", 1), ("emoji", 4), ("cjk", 3)):
+        nbytes = 48 << 20
+        n_units = nbytes // 2 if utf16 else nbytes
+        d_src = corpus.generate(profile, n_units, seed, utf16=utf16, device=dev)
+        h_src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        h_src.copy_(d_src.view(torch.uint8).cpu())
+        cap = 3 * n_units if utf16 else n_units
+        out_bytes = cap if utf16 else 2 * cap
+        h_out = torch.empty(out_bytes, dtype=torch.uint8).pin_memory()
+        d_out = torch.empty(out_bytes, dtype=torch.uint8, device=dev)
+        ws = torch.empty(_native.workspace_bytes(op, n_units) // 8 + 1, dtype=torch.int64, device=dev)
+        res_h = torch.empty(3, dtype=torch.int64, device=dev)
+        res_d = torch.empty(3, dtype=torch.int64, device=dev)
+        s = torch.cuda.current_stream(dev)
+        view = (lambda t: t) if utf16 else (lambda t: t.view(torch.int16))
+        src_view = (lambda t: t.view(torch.int16)) if utf16 else (lambda t: t)
+        _native.launch(op, src_view(d_src.view(torch.uint8)), n_units, view(d_out), cap, ws, res_d, s)
+        for _ in range(3):
+            _native.launch(op, src_view(h_src), n_units, view(h_out), cap, ws, res_h, s)
+            torch.cuda.synchronize()
+            assert res_h.cpu().tolist() == res_d.cpu().tolist()
+        w = int(res_d[2]) * (1 if utf16 else 2)
+        assert torch.equal(h_out[:w], d_out[:w].cpu())
