@@ -3,8 +3,8 @@
 // Geometry (all kernels): a warp owns a contiguous 2 KiB chunk of input and
 // walks it in 4 rounds of 512 B, lane l holding bytes [16l, 16l+16) of the
 // round in registers (neighbours by shuffle).  The transcode kernels group 4
-// chunks into an 8 KiB tile; tiles are ordered by a central scanner warp
-// (scan_tiles) rather than a per-tile look-back.
+// chunks into an 8 KiB tile; tiles are ordered by the central scanner
+// (scan_windows, the warps of CTA 0) rather than a per-tile look-back.
 //
 // Tile status word (uint64, one per tile, zeroed before each launch):
 //   bits 63..62  flag: 0 not ready, 1 aggregate, 2 exclusive prefix

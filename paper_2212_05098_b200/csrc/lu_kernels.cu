@@ -1,10 +1,10 @@
 // lu_kernels.cu -- sm_100a kernels K1..K4 and the C-ABI entry points of
 // liblaneutf_b200.so (declared in include/laneutf_b200.h).
 //
-// One launch per call: K1/K2 are single-pass (classify/validate -> decoupled
-// look-back scan -> scatter) over 16 KiB tiles; K3/K4 are read-only
-// validators that reduce the first bad position with one atomic per
-// erroneous tile and finalize in the last CTA.  Stream-ordered; the library
+// One launch per call: K1/K2 are single-pass (classify/validate -> central
+// scanner orders 8 KiB tiles -> staged scatter) persistent kernels; K3/K4 are
+// warp-persistent read-only validators that reduce the first bad position
+// with one atomic and finalize in the last warp.  Stream-ordered; the library
 // allocates nothing and keeps no mutable global state (per-call workspace,
 // thread-local error string).
 #include <cstdio>
@@ -150,18 +150,18 @@ __device__ __forceinline__ void sel_table_init(SelPair *sel)
 
 // ====================================================== pipelined transcode
 //
-// Persistent CTAs (grid = resident capacity).  A CTA holds two independent
-// tile groups of 4 compute warps each (8 KiB tiles) plus one extra warp that,
-// in CTA 0 only, runs the central scanner (scan_tiles).  Each group claims
-// tiles from a ticket counter just before computing them (tiles finish
-// roughly in ticket order), computes a tile into one of its two shared staging
-// buffers and publishes the tile aggregate; it copies a buffer out when it is
-// about to reuse it, two tiles later, by which time the scanner has normally
-// published that tile's exclusive prefix.  The two groups run unsynchronised,
-// so one group's HBM-bound copy-out overlaps the other's ALU-bound compute
-// (with a single 8-warp group the CTA alternated between the two phases and
-// they did not overlap).  Every CTA is resident and a tile publishes its
-// aggregate before waiting on anything, so progress is guaranteed.
+// Persistent CTAs (grid = resident capacity + 1).  CTA 0 runs the central
+// scanner (scan_windows) on all its warps.  Every other CTA holds two
+// independent tile groups of 4 warps (8 KiB tiles).  Each group claims tiles
+// from a ticket counter (tiles finish roughly in ticket order), computes a
+// tile into one of its two shared staging buffers and publishes the tile
+// aggregate; it copies a buffer out when it is about to reuse it, two tiles
+// later, by which time the scanner has normally published that tile's
+// exclusive prefix.  The two groups run unsynchronised, so one group's
+// HBM-bound copy-out overlaps the other's ALU-bound compute.  Every CTA is
+// resident and a tile publishes its aggregate before its group waits on
+// anything, and the scanner's partial-window fallback makes every prefix
+// depend only on earlier tiles, so progress is guaranteed.
 //
 // Named barriers per group g (kGroupThreads threads): 1+3g ticket broadcast,
 // 2+3g tile computed, 3+3g prefix broadcast.
