@@ -16,6 +16,12 @@
  *                        scalar.validate_utf8, scalar.py:150-197
  *   lu_validate_utf16le  engine.validate(UTF16_TO_UTF8, ...)    engine.py:226-240;
  *                        scalar.validate_utf16le, scalar.py:200-217
+ *   lu_utf16_length_from_utf8    scalar.utf16_length_from_utf8,
+ *                        scalar.py:220-225 (status + exact word count)
+ *   lu_utf8_length_from_utf16le  scalar.utf8_length_from_utf16le,
+ *                        scalar.py:228-233 (status + exact byte count)
+ *   lu_utf8_char_count   scalar.utf8_char_count, scalar.py:246-248
+ *   lu_utf16le_char_count scalar.utf16le_char_count, scalar.py:251-257
  *   lu_workspace_bytes   (new) sizing helper; the output sizing rule is
  *                        engine.worst_case_output_bytes, engine.py:171-175
  *   lu_device_supported  engine.detect() capability probe, engine.py:141-153
@@ -28,7 +34,9 @@
  *     meaning (outcome.py:57-83): status 0 OK, 1 MALFORMED_INPUT;
  *     ``consumed`` counts input units (bytes / 16-bit words) before the first
  *     invalid unit (== the error offset); ``written`` counts output units
- *     (16-bit words / bytes).  Validators always report written = 0.
+ *     (16-bit words / bytes).  Validators always report written = 0; the
+ *     length functions report the output length of the whole input in
+ *     ``written`` when it is valid (0 when malformed: the reference raises).
  *   - Output buffers must hold the worst case (1 word per UTF-8 byte, 3 bytes
  *     per UTF-16 word).  Exactly out[0 .. written) is written; nothing past
  *     it (the reference's canary contract).
@@ -61,7 +69,11 @@ enum {
     LU_OP_UTF8_TO_UTF16LE = 0,
     LU_OP_UTF16LE_TO_UTF8 = 1,
     LU_OP_VALIDATE_UTF8 = 2,
-    LU_OP_VALIDATE_UTF16LE = 3
+    LU_OP_VALIDATE_UTF16LE = 3,
+    LU_OP_UTF16_LENGTH_FROM_UTF8 = 4,
+    LU_OP_UTF8_LENGTH_FROM_UTF16LE = 5,
+    LU_OP_UTF8_CHAR_COUNT = 6,
+    LU_OP_UTF16LE_CHAR_COUNT = 7
 };
 
 enum {
@@ -83,6 +95,20 @@ int lu_validate_utf8(const uint8_t *in, uint64_t n_bytes, void *ws, uint64_t ws_
 
 int lu_validate_utf16le(const uint16_t *in, uint64_t n_words, void *ws, uint64_t ws_bytes, lu_outcome *res,
                         lu_stream_t stream);
+
+/* Validate and count in one pass (the validators plus a per-warp reduction). */
+int lu_utf16_length_from_utf8(const uint8_t *in, uint64_t n_bytes, void *ws, uint64_t ws_bytes, lu_outcome *res,
+                              lu_stream_t stream);
+
+int lu_utf8_length_from_utf16le(const uint16_t *in, uint64_t n_words, void *ws, uint64_t ws_bytes, lu_outcome *res,
+                                lu_stream_t stream);
+
+/* Character counts (no validation); *count is a device uint64. */
+int lu_utf8_char_count(const uint8_t *in, uint64_t n_bytes, void *ws, uint64_t ws_bytes, uint64_t *count,
+                       lu_stream_t stream);
+
+int lu_utf16le_char_count(const uint16_t *in, uint64_t n_words, void *ws, uint64_t ws_bytes, uint64_t *count,
+                          lu_stream_t stream);
 
 uint64_t lu_workspace_bytes(int op, uint64_t n_units);
 

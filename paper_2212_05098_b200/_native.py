@@ -25,6 +25,10 @@ __all__ = [
     "OP_UTF16LE_TO_UTF8",
     "OP_VALIDATE_UTF8",
     "OP_VALIDATE_UTF16LE",
+    "OP_UTF16_LENGTH_FROM_UTF8",
+    "OP_UTF8_LENGTH_FROM_UTF16LE",
+    "OP_UTF8_CHAR_COUNT",
+    "OP_UTF16LE_CHAR_COUNT",
     "workspace_bytes",
     "launch",
 ]
@@ -35,6 +39,10 @@ OP_UTF8_TO_UTF16LE = 0
 OP_UTF16LE_TO_UTF8 = 1
 OP_VALIDATE_UTF8 = 2
 OP_VALIDATE_UTF16LE = 3
+OP_UTF16_LENGTH_FROM_UTF8 = 4
+OP_UTF8_LENGTH_FROM_UTF16LE = 5
+OP_UTF8_CHAR_COUNT = 6
+OP_UTF16LE_CHAR_COUNT = 7
 
 # C ABI symbols, in header order (tests check the .so exports all of them)
 SYMBOLS = (
@@ -42,6 +50,10 @@ SYMBOLS = (
     "lu_utf16le_to_utf8",
     "lu_validate_utf8",
     "lu_validate_utf16le",
+    "lu_utf16_length_from_utf8",
+    "lu_utf8_length_from_utf16le",
+    "lu_utf8_char_count",
+    "lu_utf16le_char_count",
     "lu_workspace_bytes",
     "lu_device_supported",
     "lu_tile_bytes",
@@ -81,7 +93,8 @@ def lib():
                 fn = getattr(L, name)
                 fn.argtypes = [vp, u64, vp, u64, vp, u64, vp, vp]
                 fn.restype = i32
-            for name in ("lu_validate_utf8", "lu_validate_utf16le"):
+            for name in ("lu_validate_utf8", "lu_validate_utf16le", "lu_utf16_length_from_utf8",
+                         "lu_utf8_length_from_utf16le", "lu_utf8_char_count", "lu_utf16le_char_count"):
                 fn = getattr(L, name)
                 fn.argtypes = [vp, u64, vp, u64, vp, vp]
                 fn.restype = i32
@@ -148,7 +161,8 @@ def launch(
     """Enqueue one kernel call on ``stream`` (default: current stream).
 
     ``src``/``out``/``ws``/``res`` are CUDA tensors; ``res`` holds one
-    lu_outcome (>= 24 bytes, 8-byte aligned).  Returns without synchronising.
+    lu_outcome (>= 24 bytes, 8-byte aligned), or for the char-count ops one
+    uint64 count (``out`` unused).  Returns without synchronising.
     """
     L = lib()
     s = stream if stream is not None else torch.cuda.current_stream(src.device)
@@ -162,6 +176,14 @@ def launch(
         rc = L.lu_validate_utf8(_ptr(src), n_units, _ptr(ws), wsb, _ptr(res), sp)
     elif op == OP_VALIDATE_UTF16LE:
         rc = L.lu_validate_utf16le(_ptr(src), n_units, _ptr(ws), wsb, _ptr(res), sp)
+    elif op == OP_UTF16_LENGTH_FROM_UTF8:
+        rc = L.lu_utf16_length_from_utf8(_ptr(src), n_units, _ptr(ws), wsb, _ptr(res), sp)
+    elif op == OP_UTF8_LENGTH_FROM_UTF16LE:
+        rc = L.lu_utf8_length_from_utf16le(_ptr(src), n_units, _ptr(ws), wsb, _ptr(res), sp)
+    elif op == OP_UTF8_CHAR_COUNT:
+        rc = L.lu_utf8_char_count(_ptr(src), n_units, _ptr(ws), wsb, _ptr(res), sp)
+    elif op == OP_UTF16LE_CHAR_COUNT:
+        rc = L.lu_utf16le_char_count(_ptr(src), n_units, _ptr(ws), wsb, _ptr(res), sp)
     else:
         raise ValueError(f"unknown op {op}")
     _check(rc)

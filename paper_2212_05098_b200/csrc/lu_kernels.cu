@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
 // too).  The last warp to finish writes the result record.
 // ws layout: [u64 max(n - bad_pos)][u32 warps done][u32 pad].
 
-template <bool Utf16>
+template <bool Utf16, bool Count = false>
 __global__ void __launch_bounds__(kThreads) k_validate_w(const uint8_t *__restrict__ base, uint32_t lead,
                                                          uint64_t n, uint64_t *__restrict__ ws,
                                                          Outcome *__restrict__ res, uint64_t nchunks)
@@ -426,7 +426,8 @@ __global__ void __launch_bounds__(kThreads) k_validate_w(const uint8_t *__restri
     const uint64_t total_warps = (uint64_t)gridDim.x * kWarps;
     const uint64_t n_bytes = Utf16 ? 2 * n : n;
     const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n_bytes;
-    uint64_t best = 0; // cached global max(n - bad_pos)
+    uint64_t best = 0;  // cached global max(n - bad_pos)
+    uint32_t count = 0; // Count: this lane's output units over the warp's chunks
     // (a cp.async double buffer per warp measured 6-11% slower: the loads are
     // already latency-hidden by 32 resident warps per SM)
     for (uint64_t c = (uint64_t)blockIdx.x * kWarps + warp; c < nchunks; c += total_warps) {
@@ -435,21 +436,22 @@ __global__ void __launch_bounds__(kThreads) k_validate_w(const uint8_t *__restri
             break; // an earlier error is already known
         const uint64_t best_next = *reinterpret_cast<volatile uint64_t *>(ws); // consumed next iteration
         const bool interior = (off - 4 >= lo_b) && (off + kChunkBytes + 4 <= hi_b);
-        uint32_t err, pos;
+        uint32_t err, pos, cc = 0;
         if (Utf16) {
             if (interior)
-                u16val_warp_r<false>(base, off, lo_b, hi_b, err, pos);
+                u16val_warp_r<false, Count>(base, off, lo_b, hi_b, err, pos, &cc);
             else
-                u16val_warp_r<true>(base, off, lo_b, hi_b, err, pos);
+                u16val_warp_r<true, Count>(base, off, lo_b, hi_b, err, pos, &cc);
         } else {
             if (interior)
-                u8val_warp<false>(base, off, lo_b, hi_b, wr_s[warp], 0);
+                u8val_warp<false, Count>(base, off, lo_b, hi_b, wr_s[warp], 0, &cc);
             else
-                u8val_warp<true>(base, off, lo_b, hi_b, wr_s[warp], 0);
+                u8val_warp<true, Count>(base, off, lo_b, hi_b, wr_s[warp], 0, &cc);
             __syncwarp();
             err = wr_s[warp].err;
             pos = wr_s[warp].pos;
         }
+        count += cc;
         if (err) {
             if (lane == 0) {
                 const int64_t pb = off + pos - lo_b;
@@ -460,6 +462,11 @@ __global__ void __launch_bounds__(kThreads) k_validate_w(const uint8_t *__restri
         }
         best = best_next;
     }
+    if (Count) {
+        const uint32_t wsum = __reduce_add_sync(0xffffffffu, count);
+        if (lane == 0 && wsum)
+            atomicAdd(reinterpret_cast<unsigned long long *>(ws + 2), (unsigned long long)wsum);
+    }
     if (lane == 0) {
         __threadfence();
         const unsigned int prev = atomicAdd(reinterpret_cast<unsigned int *>(ws + 1), 1u);
@@ -469,7 +476,66 @@ __global__ void __launch_bounds__(kThreads) k_validate_w(const uint8_t *__restri
             res->status = b ? kStatusMalformed : kStatusOk;
             res->pad = 0;
             res->consumed = n - b;
-            res->written = 0;
+            res->written = (Count && !b) ? atomicAdd(reinterpret_cast<unsigned long long *>(ws + 2), 0ull) : 0;
+        }
+    }
+}
+
+// ============================================================ char counts
+//
+// utf8_char_count / utf16le_char_count (scalar.py:246-257): bytes that are
+// not continuations, or words minus low surrogates.  No validation.  A plain
+// HBM-bound reduction: 16 bytes per thread per step, one atomic per warp.
+// ws layout: [u64 sum][u32 warps done][u32 pad].
+template <bool Utf16>
+__global__ void __launch_bounds__(kThreads) k_chars(const uint8_t *__restrict__ base, uint32_t lead, uint64_t n,
+                                                    uint64_t *__restrict__ ws, uint64_t *__restrict__ out,
+                                                    uint64_t nvec)
+{
+    const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)(Utf16 ? 2 * n : n);
+    const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+    uint64_t acc = 0;
+    for (uint64_t v = (uint64_t)blockIdx.x * kThreads + threadIdx.x; v < nvec; v += stride) {
+        const int64_t a = (int64_t)v * 16;
+        const bool full = a >= lo_b && a + 16 <= hi_b;
+        const uint4 q =
+            full ? __ldcs(reinterpret_cast<const uint4 *>(base + a)) : load_u128_masked(base, a, lo_b, hi_b);
+        const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+        uint32_t c = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t x = w4[k];
+            if (Utf16) {
+                uint32_t hs, ls;
+                u16_sur_masks(x, hs, ls);
+                if (!full) {
+                    const uint32_t vw = valid_words(a + 4 * k, lo_b, hi_b);
+                    ls &= ((vw & 1) ? 0x8000u : 0u) | ((vw & 2) ? 0x80000000u : 0u);
+                }
+                c += __popc(ls);
+            } else {
+                uint32_t nc = ~(x & ~(x << 1)) & H8; // not a continuation byte
+                if (!full)
+                    nc &= valid_mask(a + 4 * k, lo_b, hi_b);
+                c += __popc(nc);
+            }
+        }
+        acc += c;
+    }
+    const uint32_t lane = lane_id();
+    unsigned long long wsum = acc;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1)
+        wsum += __shfl_down_sync(0xffffffffu, wsum, d);
+    if (lane == 0) {
+        if (wsum)
+            atomicAdd(reinterpret_cast<unsigned long long *>(ws), wsum);
+        __threadfence();
+        const unsigned int prev = atomicAdd(reinterpret_cast<unsigned int *>(ws + 1), 1u);
+        if (prev == (uint64_t)gridDim.x * kWarps - 1) {
+            __threadfence();
+            const uint64_t t = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 0ull);
+            *out = Utf16 ? n - t : t;
         }
     }
 }
@@ -538,6 +604,88 @@ static int persistent_grid(const void *fn, int threads, size_t smem, uint64_t nt
 
 using namespace lu;
 
+template <bool Utf16, bool Count>
+static int launch_validate(const uint8_t *base, uint32_t lead, uint64_t n_units, void *ws, lu_outcome *res,
+                           uint64_t nchunks, cudaStream_t stream)
+{
+    unsigned grid = 0;
+    int rc = persistent_grid((const void *)k_validate_w<Utf16, Count>, kThreads, 0, (nchunks + kWarps - 1) / kWarps,
+                             &grid);
+    if (rc)
+        return rc;
+    k_validate_w<Utf16, Count><<<grid, kThreads, 0, stream>>>(base, lead, n_units, reinterpret_cast<uint64_t *>(ws),
+                                                              reinterpret_cast<Outcome *>(res), nchunks);
+    return 0;
+}
+
+// Validators (count = false) and the validate+count length functions.
+static int validate_impl(bool utf16, bool count, const uint8_t *inb, uint64_t n_units, void *ws, uint64_t ws_bytes,
+                         lu_outcome *res, cudaStream_t stream)
+{
+    if ((!inb && n_units) || !res || !ws)
+        return fail(LU_ERR_INVALID, "null pointer");
+    if ((utf16 && ((uintptr_t)inb & 1)) || ((uintptr_t)ws & 7) || ((uintptr_t)res & 7))
+        return fail(LU_ERR_INVALID, "misaligned in/ws/res pointer");
+    if (ws_bytes < 24)
+        return fail(LU_ERR_WORKSPACE, "workspace too small (see lu_workspace_bytes)");
+    const uint32_t lead = (uint32_t)((uintptr_t)inb & 15);
+    const uint64_t nt = n_tiles(utf16 ? 2 * n_units : n_units, lead);
+    if (nt > 0x7fffffffull)
+        return fail(LU_ERR_INVALID, "input too large");
+    cudaError_t e = cudaMemsetAsync(ws, 0, 24, stream);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "cudaMemsetAsync");
+    const uint8_t *base = inb ? inb - lead : reinterpret_cast<const uint8_t *>(16);
+    const uint64_t nchunks = n_tiles(utf16 ? 2 * n_units : n_units, lead, kChunkBytes);
+    int rc;
+    if (utf16)
+        rc = count ? launch_validate<true, true>(base, lead, n_units, ws, res, nchunks, stream)
+                   : launch_validate<true, false>(base, lead, n_units, ws, res, nchunks, stream);
+    else
+        rc = count ? launch_validate<false, true>(base, lead, n_units, ws, res, nchunks, stream)
+                   : launch_validate<false, false>(base, lead, n_units, ws, res, nchunks, stream);
+    if (rc)
+        return rc;
+    e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return cuda_fail(e, "k_validate launch");
+    return 0;
+}
+
+static int chars_impl(bool utf16, const uint8_t *inb, uint64_t n_units, void *ws, uint64_t ws_bytes, uint64_t *count,
+                      cudaStream_t stream)
+{
+    if ((!inb && n_units) || !count || !ws)
+        return fail(LU_ERR_INVALID, "null pointer");
+    if ((utf16 && ((uintptr_t)inb & 1)) || ((uintptr_t)ws & 7) || ((uintptr_t)count & 7))
+        return fail(LU_ERR_INVALID, "misaligned in/ws/count pointer");
+    if (ws_bytes < 16)
+        return fail(LU_ERR_WORKSPACE, "workspace too small (see lu_workspace_bytes)");
+    const uint32_t lead = (uint32_t)((uintptr_t)inb & 15);
+    const uint64_t nbytes = utf16 ? 2 * n_units : n_units;
+    cudaError_t e = cudaMemsetAsync(ws, 0, 16, stream);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "cudaMemsetAsync");
+    const uint8_t *base = inb ? inb - lead : reinterpret_cast<const uint8_t *>(16);
+    const uint64_t nvec = (lead + nbytes + 15) / 16;
+    unsigned grid = 0;
+    const void *fn = utf16 ? (const void *)k_chars<true> : (const void *)k_chars<false>;
+    // at least one CTA: its last warp writes the result (0 for empty input)
+    int rc = persistent_grid(fn, kThreads, 0, nvec ? (nvec + kThreads - 1) / kThreads : 1, &grid);
+    if (rc)
+        return rc;
+    if (utf16)
+        k_chars<true><<<grid, kThreads, 0, stream>>>(base, lead, n_units, reinterpret_cast<uint64_t *>(ws), count,
+                                                     nvec);
+    else
+        k_chars<false><<<grid, kThreads, 0, stream>>>(base, lead, n_units, reinterpret_cast<uint64_t *>(ws), count,
+                                                      nvec);
+    e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return cuda_fail(e, "k_chars launch");
+    return 0;
+}
+
 extern "C" {
 
 const char *lu_last_error(void) { return g_err.c_str(); }
@@ -565,6 +713,10 @@ uint64_t lu_workspace_bytes(int op, uint64_t n_units)
         return 8 * (n_tiles(2 * n_units, 15, kPipeTile) + 1) + 64;
     case LU_OP_VALIDATE_UTF8:
     case LU_OP_VALIDATE_UTF16LE:
+    case LU_OP_UTF16_LENGTH_FROM_UTF8:
+    case LU_OP_UTF8_LENGTH_FROM_UTF16LE:
+    case LU_OP_UTF8_CHAR_COUNT:
+    case LU_OP_UTF16LE_CHAR_COUNT:
         return 64;
     default:
         return 0;
@@ -661,54 +813,40 @@ int lu_utf16le_to_utf8(const uint16_t *in, uint64_t n_words, uint8_t *out, uint6
     return 0;
 }
 
-static int validate_impl(bool utf16, const uint8_t *inb, uint64_t n_units, void *ws, uint64_t ws_bytes,
-                         lu_outcome *res, cudaStream_t stream)
-{
-    if ((!inb && n_units) || !res || !ws)
-        return fail(LU_ERR_INVALID, "null pointer");
-    if ((utf16 && ((uintptr_t)inb & 1)) || ((uintptr_t)ws & 7) || ((uintptr_t)res & 7))
-        return fail(LU_ERR_INVALID, "misaligned in/ws/res pointer");
-    if (ws_bytes < 16)
-        return fail(LU_ERR_WORKSPACE, "workspace too small (see lu_workspace_bytes)");
-    const uint32_t lead = (uint32_t)((uintptr_t)inb & 15);
-    const uint64_t nt = n_tiles(utf16 ? 2 * n_units : n_units, lead);
-    if (nt > 0x7fffffffull)
-        return fail(LU_ERR_INVALID, "input too large");
-    int rc = set_smem_attrs();
-    if (rc)
-        return rc;
-    cudaError_t e = cudaMemsetAsync(ws, 0, 16, stream);
-    if (e != cudaSuccess)
-        return cuda_fail(e, "cudaMemsetAsync");
-    const uint8_t *base = inb ? inb - lead : reinterpret_cast<const uint8_t *>(16);
-    const uint64_t nchunks = n_tiles(utf16 ? 2 * n_units : n_units, lead, kChunkBytes);
-    unsigned grid = 0;
-    rc = persistent_grid(utf16 ? (const void *)k_validate_w<true> : (const void *)k_validate_w<false>, kThreads, 0,
-                         (nchunks + kWarps - 1) / kWarps, &grid);
-    if (rc)
-        return rc;
-    if (utf16)
-        k_validate_w<true><<<grid, kThreads, 0, stream>>>(base, lead, n_units, reinterpret_cast<uint64_t *>(ws),
-                                                          reinterpret_cast<Outcome *>(res), nchunks);
-    else
-        k_validate_w<false><<<grid, kThreads, 0, stream>>>(base, lead, n_units, reinterpret_cast<uint64_t *>(ws),
-                                                           reinterpret_cast<Outcome *>(res), nchunks);
-    e = cudaGetLastError();
-    if (e != cudaSuccess)
-        return cuda_fail(e, "k_validate launch");
-    return 0;
-}
-
 int lu_validate_utf8(const uint8_t *in, uint64_t n_bytes, void *ws, uint64_t ws_bytes, lu_outcome *res,
                      cudaStream_t stream)
 {
-    return validate_impl(false, in, n_bytes, ws, ws_bytes, res, stream);
+    return validate_impl(false, false, in, n_bytes, ws, ws_bytes, res, stream);
 }
 
 int lu_validate_utf16le(const uint16_t *in, uint64_t n_words, void *ws, uint64_t ws_bytes, lu_outcome *res,
                         cudaStream_t stream)
 {
-    return validate_impl(true, reinterpret_cast<const uint8_t *>(in), n_words, ws, ws_bytes, res, stream);
+    return validate_impl(true, false, reinterpret_cast<const uint8_t *>(in), n_words, ws, ws_bytes, res, stream);
+}
+
+int lu_utf16_length_from_utf8(const uint8_t *in, uint64_t n_bytes, void *ws, uint64_t ws_bytes, lu_outcome *res,
+                              cudaStream_t stream)
+{
+    return validate_impl(false, true, in, n_bytes, ws, ws_bytes, res, stream);
+}
+
+int lu_utf8_length_from_utf16le(const uint16_t *in, uint64_t n_words, void *ws, uint64_t ws_bytes, lu_outcome *res,
+                                cudaStream_t stream)
+{
+    return validate_impl(true, true, reinterpret_cast<const uint8_t *>(in), n_words, ws, ws_bytes, res, stream);
+}
+
+int lu_utf8_char_count(const uint8_t *in, uint64_t n_bytes, void *ws, uint64_t ws_bytes, uint64_t *count,
+                       cudaStream_t stream)
+{
+    return chars_impl(false, in, n_bytes, ws, ws_bytes, count, stream);
+}
+
+int lu_utf16le_char_count(const uint16_t *in, uint64_t n_words, void *ws, uint64_t ws_bytes, uint64_t *count,
+                          cudaStream_t stream)
+{
+    return chars_impl(true, reinterpret_cast<const uint8_t *>(in), n_words, ws, ws_bytes, count, stream);
 }
 
 } // extern "C"

@@ -233,35 +233,23 @@ __device__ __forceinline__ void u16_sur_masks(uint32_t x, uint32_t &hs, uint32_t
 // exactly where the previous word is a high surrogate, so the round is clean
 // iff ls == hs shifted by one word (one funnel shift per quad); a flagged
 // round is resolved with the exact predicate u16_bad2.
-template <bool Boundary>
+// Count = true also returns, in `count`, the UTF-8 length of the chunk's
+// words (1/2/3 bytes per BMP word, 4 per high surrogate, 0 per low one; exact
+// when the input is valid) -- utf8_length_from_utf16le.
+template <bool Boundary, bool Count = false>
 __device__ __forceinline__ void u16val_warp_r(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
-                                              int64_t hi_b, uint32_t &err, uint32_t &err_pos)
+                                              int64_t hi_b, uint32_t &err, uint32_t &err_pos,
+                                              uint32_t *count = nullptr)
 {
     const uint32_t lane = lane_id();
     const int64_t chunk = tile_off;
     constexpr int kRounds = kChunkBytes / 512;
-    uint4 q[kRounds];
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
-        const int64_t a = chunk + r * 512 + 16 * (int64_t)lane;
-        if (!Boundary)
-            q[r] = __ldcs(reinterpret_cast<const uint4 *>(base + a));
-        else if (a + 16 <= lo_b || a >= hi_b)
-            q[r] = make_uint4(0, 0, 0, 0);
-        else
-            q[r] = load_u128_masked(base, a, lo_b, hi_b);
-    }
-    uint32_t carry = 0, halo_n = 0;
-    if (lane == 0) {
-        const int64_t a = chunk - 4;
-        carry = Boundary ? ((a + 4 <= lo_b || a >= hi_b) ? 0u : load_u32_masked(base, a, lo_b, hi_b))
-                         : __ldg(reinterpret_cast<const uint32_t *>(base + a));
-    }
-    if (lane == 31) {
-        const int64_t a = chunk + kChunkBytes;
-        halo_n = Boundary ? ((a + 4 <= lo_b || a >= hi_b) ? 0u : load_u32_masked(base, a, lo_b, hi_b))
-                          : __ldg(reinterpret_cast<const uint32_t *>(base + a));
-    }
+    ChunkIn in;
+    load_chunk<Boundary>(base, chunk, lo_b, hi_b, in);
+    const uint4 *q = in.q;
+    uint32_t carry = in.halo_p;
+    const uint32_t halo_n = in.halo_n;
+    uint32_t cnt = 0;
     uint32_t rn[kRounds];
 #pragma unroll
     for (int r = 0; r < kRounds; ++r)
@@ -287,6 +275,22 @@ __device__ __forceinline__ void u16val_warp_r(const uint8_t *__restrict__ base, 
 #pragma unroll
         for (int k = 1; k <= 5; ++k)
             det |= ls[k] ^ fsl(hs[k - 1], hs[k], 16);
+        if (Count) {
+#pragma unroll
+            for (int k = 1; k <= 4; ++k) {
+                const uint32_t x = w[k];
+                const uint32_t a = x & 0xFF80FF80u, b = x & 0xF800F800u;
+                const uint32_t big = (((a & 0x7FFF7FFFu) + 0x7FFF7FFFu) | a) & 0x80008000u; // word >= 0x80
+                const uint32_t mid = (((b & 0x7FFF7FFFu) + 0x7FFF7FFFu) | b) & 0x80008000u; // word >= 0x800
+                uint32_t one = 0x80008000u;
+                if (Boundary) {
+                    const uint32_t v = valid_words(chunk + r * 512 + 16 * (int64_t)lane + 4 * (k - 1), lo_b, hi_b);
+                    one = ((v & 1) ? 0x8000u : 0u) | ((v & 2) ? 0x80000000u : 0u);
+                }
+                // out-of-range words read as 0: no big/mid/surrogate bits
+                cnt += __popc(one) + __popc(big) + __popc(mid) + __popc(hs[k]) - 3 * __popc(ls[k]);
+            }
+        }
         if (__any_sync(0xffffffffu, det != 0)) {
             const int64_t lane_off = chunk + r * 512 + 16 * (int64_t)lane;
             uint32_t kb = 8;
@@ -307,6 +311,8 @@ __device__ __forceinline__ void u16val_warp_r(const uint8_t *__restrict__ base, 
             }
         }
     }
+    if (Count)
+        *count = cnt;
 }
 
 } // namespace lu

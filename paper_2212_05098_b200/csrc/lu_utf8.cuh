@@ -522,10 +522,15 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
 
 // ============================================================ K3: validate
 
-template <bool Boundary>
+// Count = true also returns, in `count`, the UTF-16 length of the chunk
+// (one word per non-continuation byte plus one per 4-byte lead; exact when the
+// input is valid) -- utf16_length_from_utf8.
+template <bool Boundary, bool Count = false>
 __device__ __forceinline__ void u8val_warp(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
-                                           int64_t hi_b, WarpResult &wr, uint32_t warp /* warp index in tile */)
+                                           int64_t hi_b, WarpResult &wr, uint32_t warp /* warp index in tile */,
+                                           uint32_t *count = nullptr)
 {
+    uint32_t cnt = 0;
     const uint32_t lane = lane_id();
     const int64_t chunk = tile_off + (int64_t)warp * kChunkBytes;
     constexpr int kRounds = kChunkBytes / 512;
@@ -556,6 +561,15 @@ __device__ __forceinline__ void u8val_warp(const uint8_t *__restrict__ base, int
             const uint32_t cn = u8_classify(R.w[5]).C;
             const U8Masks &m = R.m[4];
             R.det |= (m.L & ~fsr(m.C, cn, 8)) | (m.E & ~fsr(m.C, cn, 16)) | (m.F & ~fsr(m.C, cn, 24));
+        }
+        if (Count) {
+#pragma unroll
+            for (int k = 1; k <= 4; ++k) {
+                uint32_t vm = H8;
+                if (Boundary)
+                    vm = valid_mask(chunk + r * 512 + 16 * (int64_t)lane + 4 * (k - 1), lo_b, hi_b);
+                cnt += __popc(~R.m[k].C & vm) + __popc(R.m[k].F & vm);
+            }
         }
         if (__any_sync(0xffffffffu, R.det != 0)) {
             const int64_t rstart = chunk + r * 512;
@@ -597,6 +611,8 @@ __device__ __forceinline__ void u8val_warp(const uint8_t *__restrict__ base, int
         wr.pos = err_pos;
         wr.units = 0;
     }
+    if (Count)
+        *count = cnt;
 }
 
 } // namespace lu

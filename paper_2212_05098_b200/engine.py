@@ -56,6 +56,11 @@ __all__ = [
     "outcome_from_tensor",
     "swap_utf16_byte_order",
     "worst_case_output_bytes",
+    "utf16_length_from_utf8",
+    "utf8_length_from_utf16le",
+    "utf8_char_count",
+    "utf16le_char_count",
+    "count_device",
 ]
 
 UTF8_TO_UTF16 = "utf8-to-utf16"
@@ -391,6 +396,62 @@ def validate(
     res = validate_device(direction, src)
     outcome = outcome_from_tensor(res.cpu())
     return TranscodeOutcome(outcome.status, outcome.consumed, 0)
+
+
+# ------------------------------------------- lengths and char counts (8f)
+
+
+def count_device(op: int, src: torch.Tensor, *, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
+    """Enqueue a length (validate + count) or char-count op on a CUDA uint8
+    tensor; returns the int64 result tensor (lu_outcome[3] for the length ops,
+    [1] count for the char counts).  No synchronisation."""
+    srcb = _to_device_bytes(src, src.device)
+    nbytes = srcb.numel()
+    utf16 = op in (_native.OP_UTF8_LENGTH_FROM_UTF16LE, _native.OP_UTF16LE_CHAR_COUNT)
+    if utf16 and nbytes % 2:
+        raise ValueError("UTF-16 input must be an even number of bytes")
+    n_units = nbytes // 2 if utf16 else nbytes
+    chars = op in (_native.OP_UTF8_CHAR_COUNT, _native.OP_UTF16LE_CHAR_COUNT)
+    res = torch.empty(1 if chars else 3, dtype=torch.int64, device=srcb.device)
+    ws = torch.empty(_native.workspace_bytes(op, n_units) // 8 + 1, dtype=torch.int64, device=srcb.device)
+    _native.launch(op, srcb, n_units, None, 0, ws, res, stream)
+    return res
+
+
+def _length(op: int, data, what: str, unit: str) -> int:
+    src = _to_device_bytes(data, _device())
+    outcome = outcome_from_tensor(count_device(op, src).cpu())
+    if not outcome.ok:
+        raise ValueError(f"invalid {what} at {unit} {outcome.consumed}")
+    return outcome.written
+
+
+def utf16_length_from_utf8(data) -> int:
+    """Exact UTF-16 length in words; ValueError if the input is invalid
+    (scalar.py:220-225).  One read-only pass: the K3 detectors plus a count."""
+    return _length(_native.OP_UTF16_LENGTH_FROM_UTF8, data, "UTF-8", "byte")
+
+
+def utf8_length_from_utf16le(data) -> int:
+    """Exact UTF-8 length in bytes; ValueError if the input is invalid
+    (scalar.py:228-233)."""
+    if _byte_len(data) % 2:
+        raise ValueError("UTF-16 input must be an even number of bytes")
+    return _length(_native.OP_UTF8_LENGTH_FROM_UTF16LE, data, "UTF-16", "word")
+
+
+def utf8_char_count(data) -> int:
+    """Lead and ASCII bytes, no validation (scalar.py:246-248)."""
+    src = _to_device_bytes(data, _device())
+    return int(count_device(_native.OP_UTF8_CHAR_COUNT, src).cpu()[0])
+
+
+def utf16le_char_count(data) -> int:
+    """Words minus low surrogates, no validation (scalar.py:251-257)."""
+    if _byte_len(data) % 2:
+        raise ValueError("UTF-16 input must be an even number of bytes")
+    src = _to_device_bytes(data, _device())
+    return int(count_device(_native.OP_UTF16LE_CHAR_COUNT, src).cpu()[0])
 
 
 def swap_utf16_byte_order(data: bytes) -> bytes:

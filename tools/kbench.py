@@ -16,7 +16,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2212_05098_b200 import UTF8_TO_UTF16, UTF16_TO_UTF8, _native, corpus, outcome_from_tensor  # noqa: E402
-from paper_2212_05098_b200 import transcode_device, validate_device  # noqa: E402
+from paper_2212_05098_b200 import count_device, transcode_device, validate_device  # noqa: E402
 
 PROFILES = (("latin", 1), ("cyrillic", 2), ("cjk", 3), ("emoji", 4))
 
@@ -69,6 +69,13 @@ def main():
             t = timeit(lambda: validate_device(UTF16_TO_UTF8, u16, res=res, ws=ws))
             report[f"k4_{p}"] = {"us": round(t * 1e6, 1), "gib_s": round(n / t / 2**30, 1),
                                  "frac": round(n / t / 1e9 / peak, 3)}
+            for name, op, src in (("len_u8", _native.OP_UTF16_LENGTH_FROM_UTF8, u8),
+                                  ("len_u16", _native.OP_UTF8_LENGTH_FROM_UTF16LE, u16),
+                                  ("chars_u8", _native.OP_UTF8_CHAR_COUNT, u8),
+                                  ("chars_u16", _native.OP_UTF16LE_CHAR_COUNT, u16)):
+                t = timeit(lambda: count_device(op, src))
+                report[f"{name}_{p}"] = {"us": round(t * 1e6, 1), "gib_s": round(n / t / 2**30, 1),
+                                         "frac": round(n / t / 1e9 / peak, 3)}
         del u8, u16
     print(json.dumps(report))
 
