@@ -234,6 +234,7 @@ def main():
         UTF8_TO_UTF16,
         UTF16_TO_UTF8,
         corpus,
+        count_device,
         outcome_from_tensor,
         transcode,
         transcode_device,
@@ -428,6 +429,23 @@ def main():
                         "frac_of_measured": round(BUF_BYTES / t / 1e9 / peak, 4), "ok": o.ok,
                         "control": "zero-error buffer"}
         extras["config4_validate"] = c4
+        # row 8f(4): one-pass lengths (validate + count) and char counts
+        c8 = {}
+        for name, op, buf in (("utf16_length_from_utf8_cjk", _native.OP_UTF16_LENGTH_FROM_UTF8, srcs[2]),
+                              ("utf8_length_from_utf16le_emoji", _native.OP_UTF8_LENGTH_FROM_UTF16LE, src16[3]),
+                              ("utf8_char_count_cjk", _native.OP_UTF8_CHAR_COUNT, srcs[2]),
+                              ("utf16le_char_count_emoji", _native.OP_UTF16LE_CHAR_COUNT, src16[3])):
+            count_device(op, buf)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(k_ex):
+                count_device(op, buf)
+            b.record(stream)
+            torch.cuda.synchronize()
+            t = a.elapsed_time(b) / 1e3 / k_ex
+            c8[name] = {"input_gib_s": round(BUF_BYTES / GIB / t, 2),
+                        "frac_of_measured": round(BUF_BYTES / t / 1e9 / peak, 4)}
+        extras["row8f_lengths_and_char_counts"] = c8
         line["extras"] = extras
 
     if rank == 0 and world == 1:
