@@ -446,6 +446,23 @@ def main():
             c8[name] = {"input_gib_s": round(BUF_BYTES / GIB / t, 2),
                         "frac_of_measured": round(BUF_BYTES / t / 1e9 / peak, 4)}
         extras["row8f_lengths_and_char_counts"] = c8
+        # row 8f(1): UTF-16BE, swap fused into K1's compaction / K2's load
+        c9 = {}
+        for name, direction, buf, out in (("utf8_to_utf16be_latin", UTF8_TO_UTF16, srcs[0], outs[0]),
+                                          ("utf16be_to_utf8_emoji", UTF16_TO_UTF8, src16[3], out8)):
+            res, _ = transcode_device(direction, buf, out, utf16_byte_order="be")
+            o = outcome_from_tensor(res.cpu())
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(k_ex):
+                transcode_device(direction, buf, out, res=res, utf16_byte_order="be")
+            b.record(stream)
+            torch.cuda.synchronize()
+            t = a.elapsed_time(b) / 1e3 / k_ex
+            ab = BUF_BYTES + (2 if direction == UTF8_TO_UTF16 else 1) * o.written
+            c9[name] = {"input_gib_s": round(BUF_BYTES / GIB / t, 2), "frac_of_measured": round(ab / t / 1e9 / peak, 4),
+                        "ok": o.ok, "note": "input is the LE profile buffer (BE of other text); same work"}
+        extras["row8f_utf16be"] = c9
         line["extras"] = extras
 
     if rank == 0 and world == 1:

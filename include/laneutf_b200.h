@@ -22,6 +22,8 @@
  *                        scalar.py:228-233 (status + exact byte count)
  *   lu_utf8_char_count   scalar.utf8_char_count, scalar.py:246-248
  *   lu_utf16le_char_count scalar.utf16le_char_count, scalar.py:251-257
+ *   lu_utf8_to_utf16be / lu_utf16be_to_utf8 / lu_validate_utf16be
+ *                        the CLI's utf16be formats, cli.py:90-94, 113-114
  *   lu_workspace_bytes   (new) sizing helper; the output sizing rule is
  *                        engine.worst_case_output_bytes, engine.py:171-175
  *   lu_device_supported  engine.detect() capability probe, engine.py:141-153
@@ -73,7 +75,10 @@ enum {
     LU_OP_UTF16_LENGTH_FROM_UTF8 = 4,
     LU_OP_UTF8_LENGTH_FROM_UTF16LE = 5,
     LU_OP_UTF8_CHAR_COUNT = 6,
-    LU_OP_UTF16LE_CHAR_COUNT = 7
+    LU_OP_UTF16LE_CHAR_COUNT = 7,
+    LU_OP_UTF8_TO_UTF16BE = 8,
+    LU_OP_UTF16BE_TO_UTF8 = 9,
+    LU_OP_VALIDATE_UTF16BE = 10
 };
 
 enum {
@@ -94,6 +99,19 @@ int lu_validate_utf8(const uint8_t *in, uint64_t n_bytes, void *ws, uint64_t ws_
                      lu_stream_t stream);
 
 int lu_validate_utf16le(const uint16_t *in, uint64_t n_words, void *ws, uint64_t ws_bytes, lu_outcome *res,
+                        lu_stream_t stream);
+
+/* UTF-16BE variants: identical outcomes to the LE calls on the byte-swapped
+ * buffer (the reference swaps the whole buffer in its CLI, cli.py:90-94,
+ * 113-114, with engine.swap_utf16_byte_order, engine.py:243-250); here the
+ * swap is fused into K1's compaction and K2/K4's load. */
+int lu_utf8_to_utf16be(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint64_t out_cap_words, void *ws,
+                       uint64_t ws_bytes, lu_outcome *res, lu_stream_t stream);
+
+int lu_utf16be_to_utf8(const uint16_t *in, uint64_t n_words, uint8_t *out, uint64_t out_cap_bytes, void *ws,
+                       uint64_t ws_bytes, lu_outcome *res, lu_stream_t stream);
+
+int lu_validate_utf16be(const uint16_t *in, uint64_t n_words, void *ws, uint64_t ws_bytes, lu_outcome *res,
                         lu_stream_t stream);
 
 /* Validate and count in one pass (the validators plus a per-warp reduction). */

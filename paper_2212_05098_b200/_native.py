@@ -29,6 +29,9 @@ __all__ = [
     "OP_UTF8_LENGTH_FROM_UTF16LE",
     "OP_UTF8_CHAR_COUNT",
     "OP_UTF16LE_CHAR_COUNT",
+    "OP_UTF8_TO_UTF16BE",
+    "OP_UTF16BE_TO_UTF8",
+    "OP_VALIDATE_UTF16BE",
     "workspace_bytes",
     "launch",
 ]
@@ -43,6 +46,9 @@ OP_UTF16_LENGTH_FROM_UTF8 = 4
 OP_UTF8_LENGTH_FROM_UTF16LE = 5
 OP_UTF8_CHAR_COUNT = 6
 OP_UTF16LE_CHAR_COUNT = 7
+OP_UTF8_TO_UTF16BE = 8
+OP_UTF16BE_TO_UTF8 = 9
+OP_VALIDATE_UTF16BE = 10
 
 # C ABI symbols, in header order (tests check the .so exports all of them)
 SYMBOLS = (
@@ -50,6 +56,9 @@ SYMBOLS = (
     "lu_utf16le_to_utf8",
     "lu_validate_utf8",
     "lu_validate_utf16le",
+    "lu_utf8_to_utf16be",
+    "lu_utf16be_to_utf8",
+    "lu_validate_utf16be",
     "lu_utf16_length_from_utf8",
     "lu_utf8_length_from_utf16le",
     "lu_utf8_char_count",
@@ -89,11 +98,11 @@ def lib():
                 _load_error = f"cannot load {LIB_PATH}: {exc}"
                 raise NativeUnavailable(_load_error) from exc
             vp, u64, i32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int
-            for name in ("lu_utf8_to_utf16le", "lu_utf16le_to_utf8"):
+            for name in ("lu_utf8_to_utf16le", "lu_utf16le_to_utf8", "lu_utf8_to_utf16be", "lu_utf16be_to_utf8"):
                 fn = getattr(L, name)
                 fn.argtypes = [vp, u64, vp, u64, vp, u64, vp, vp]
                 fn.restype = i32
-            for name in ("lu_validate_utf8", "lu_validate_utf16le", "lu_utf16_length_from_utf8",
+            for name in ("lu_validate_utf8", "lu_validate_utf16le", "lu_validate_utf16be", "lu_utf16_length_from_utf8",
                          "lu_utf8_length_from_utf16le", "lu_utf8_char_count", "lu_utf16le_char_count"):
                 fn = getattr(L, name)
                 fn.argtypes = [vp, u64, vp, u64, vp, vp]
@@ -176,6 +185,12 @@ def launch(
         rc = L.lu_validate_utf8(_ptr(src), n_units, _ptr(ws), wsb, _ptr(res), sp)
     elif op == OP_VALIDATE_UTF16LE:
         rc = L.lu_validate_utf16le(_ptr(src), n_units, _ptr(ws), wsb, _ptr(res), sp)
+    elif op == OP_UTF8_TO_UTF16BE:
+        rc = L.lu_utf8_to_utf16be(_ptr(src), n_units, _ptr(out), out_cap_units, _ptr(ws), wsb, _ptr(res), sp)
+    elif op == OP_UTF16BE_TO_UTF8:
+        rc = L.lu_utf16be_to_utf8(_ptr(src), n_units, _ptr(out), out_cap_units, _ptr(ws), wsb, _ptr(res), sp)
+    elif op == OP_VALIDATE_UTF16BE:
+        rc = L.lu_validate_utf16be(_ptr(src), n_units, _ptr(ws), wsb, _ptr(res), sp)
     elif op == OP_UTF16_LENGTH_FROM_UTF8:
         rc = L.lu_utf16_length_from_utf8(_ptr(src), n_units, _ptr(ws), wsb, _ptr(res), sp)
     elif op == OP_UTF8_LENGTH_FROM_UTF16LE:

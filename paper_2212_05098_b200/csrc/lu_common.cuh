@@ -335,16 +335,29 @@ struct ChunkIn {
     uint32_t halo_n; // lane 31: the 4 bytes after it
 };
 
-template <bool Boundary>
+// byte-swap both 16-bit units of a quad (UTF-16BE <-> LE)
+__device__ __forceinline__ uint32_t swap16x2(uint32_t x) { return prmt(x, 0u, 0x2301u); }
+
+// Swap16: the input is UTF-16BE; every word is byte-swapped on load so the
+// UTF-16 kernels see LE words (swap_utf16_byte_order fused into the load,
+// SURVEY 8f(1); the reference swaps the whole buffer first, cli.py:90-94).
+template <bool Boundary, bool Swap16 = false>
 __device__ __forceinline__ void load_chunk(const uint8_t *__restrict__ base, int64_t chunk, int64_t lo_b, int64_t hi_b,
                                            ChunkIn &in)
 {
     const uint32_t lane = lane_id();
 #pragma unroll
-    for (int r = 0; r < kChunkBytes / 512; ++r)
+    for (int r = 0; r < kChunkBytes / 512; ++r) {
         in.q[r] = ld16(base, chunk + r * 512 + 16 * (int64_t)lane, lo_b, hi_b, Boundary);
+        if (Swap16)
+            in.q[r] = make_uint4(swap16x2(in.q[r].x), swap16x2(in.q[r].y), swap16x2(in.q[r].z), swap16x2(in.q[r].w));
+    }
     in.halo_p = (lane == 0) ? halo4<Boundary>(base, chunk - 4, lo_b, hi_b) : 0u;
     in.halo_n = (lane == 31) ? halo4<Boundary>(base, chunk + kChunkBytes, lo_b, hi_b) : 0u;
+    if (Swap16) {
+        in.halo_p = swap16x2(in.halo_p);
+        in.halo_n = swap16x2(in.halo_n);
+    }
 }
 
 // Per-quad validity mask (bit 7 of each byte whose logical position is in

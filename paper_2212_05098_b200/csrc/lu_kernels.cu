@@ -188,8 +188,10 @@ __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n)
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// Direction traits: UTF-8 -> UTF-16 (K1) and UTF-16 -> UTF-8 (K2).
-struct DirU8U16 {
+// Direction traits: UTF-8 -> UTF-16 (K1) and UTF-16 -> UTF-8 (K2); BE = the
+// UTF-16 side is big-endian (byte swap fused into K1's compaction / K2's load).
+template <bool BE>
+struct DirU8U16T {
     using OutT = uint16_t;
     static constexpr int kStride = kOutStrideU16;
     static constexpr int kUnitShift = 0; // input positions are bytes
@@ -204,7 +206,7 @@ struct DirU8U16 {
     __device__ static void compute(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, OutT *out_w,
                                    const SelPair *sel, WarpResult &wr, uint32_t wit, const In &in)
     {
-        u8u16_warp<B>(base, tile_off, lo_b, hi_b, out_w, sel, wr, wit, in);
+        u8u16_warp<B, BE>(base, tile_off, lo_b, hi_b, out_w, sel, wr, wit, in);
     }
     __device__ static void copy_out(const OutT *src, uint32_t cnt, OutT *out_a, uint64_t g0)
     {
@@ -212,7 +214,8 @@ struct DirU8U16 {
     }
 };
 
-struct DirU16U8 {
+template <bool BE>
+struct DirU16U8T {
     using OutT = uint8_t;
     static constexpr int kStride = kOutStrideU8;
     static constexpr int kUnitShift = 1; // input positions are 16-bit words
@@ -221,7 +224,7 @@ struct DirU16U8 {
     __device__ static void load(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, uint32_t wit,
                                 In &in)
     {
-        load_chunk<B>(base, tile_off + (int64_t)wit * kChunkBytes, lo_b, hi_b, in);
+        load_chunk<B, BE>(base, tile_off + (int64_t)wit * kChunkBytes, lo_b, hi_b, in);
     }
     template <bool B>
     __device__ static void compute(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, OutT *out_w,
@@ -234,6 +237,9 @@ struct DirU16U8 {
         copy_out_u8(src, cnt, out_a, g0);
     }
 };
+
+using DirU8U16 = DirU8U16T<false>;
+using DirU16U8 = DirU16U8T<false>;
 
 // Group thread 0: wait for the scanner's exclusive prefix of the tile held in
 // buffer b, and write the result record if this is the first-error tile or
@@ -415,7 +421,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
 // too).  The last warp to finish writes the result record.
 // ws layout: [u64 max(n - bad_pos)][u32 warps done][u32 pad].
 
-template <bool Utf16, bool Count = false>
+template <bool Utf16, bool Count = false, bool Swap16 = false>
 __global__ void __launch_bounds__(kThreads) k_validate_w(const uint8_t *__restrict__ base, uint32_t lead,
                                                          uint64_t n, uint64_t *__restrict__ ws,
                                                          Outcome *__restrict__ res, uint64_t nchunks)
@@ -439,9 +445,9 @@ __global__ void __launch_bounds__(kThreads) k_validate_w(const uint8_t *__restri
         uint32_t err, pos, cc = 0;
         if (Utf16) {
             if (interior)
-                u16val_warp_r<false, Count>(base, off, lo_b, hi_b, err, pos, &cc);
+                u16val_warp_r<false, Count, Swap16>(base, off, lo_b, hi_b, err, pos, &cc);
             else
-                u16val_warp_r<true, Count>(base, off, lo_b, hi_b, err, pos, &cc);
+                u16val_warp_r<true, Count, Swap16>(base, off, lo_b, hi_b, err, pos, &cc);
         } else {
             if (interior)
                 u8val_warp<false, Count>(base, off, lo_b, hi_b, wr_s[warp], 0, &cc);
@@ -572,6 +578,12 @@ static int set_smem_attrs()
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(k_transcode<DirU16U8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kSmemK2);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_transcode<DirU8U16T<true>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSmemK1);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_transcode<DirU16U8T<true>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSmemK2);
         status = e;
     });
     if (status != cudaSuccess)
@@ -604,23 +616,23 @@ static int persistent_grid(const void *fn, int threads, size_t smem, uint64_t nt
 
 using namespace lu;
 
-template <bool Utf16, bool Count>
+template <bool Utf16, bool Count, bool Swap16 = false>
 static int launch_validate(const uint8_t *base, uint32_t lead, uint64_t n_units, void *ws, lu_outcome *res,
                            uint64_t nchunks, cudaStream_t stream)
 {
     unsigned grid = 0;
-    int rc = persistent_grid((const void *)k_validate_w<Utf16, Count>, kThreads, 0, (nchunks + kWarps - 1) / kWarps,
-                             &grid);
+    int rc = persistent_grid((const void *)k_validate_w<Utf16, Count, Swap16>, kThreads, 0,
+                             (nchunks + kWarps - 1) / kWarps, &grid);
     if (rc)
         return rc;
-    k_validate_w<Utf16, Count><<<grid, kThreads, 0, stream>>>(base, lead, n_units, reinterpret_cast<uint64_t *>(ws),
-                                                              reinterpret_cast<Outcome *>(res), nchunks);
+    k_validate_w<Utf16, Count, Swap16><<<grid, kThreads, 0, stream>>>(
+        base, lead, n_units, reinterpret_cast<uint64_t *>(ws), reinterpret_cast<Outcome *>(res), nchunks);
     return 0;
 }
 
 // Validators (count = false) and the validate+count length functions.
 static int validate_impl(bool utf16, bool count, const uint8_t *inb, uint64_t n_units, void *ws, uint64_t ws_bytes,
-                         lu_outcome *res, cudaStream_t stream)
+                         lu_outcome *res, cudaStream_t stream, bool be = false)
 {
     if ((!inb && n_units) || !res || !ws)
         return fail(LU_ERR_INVALID, "null pointer");
@@ -638,7 +650,9 @@ static int validate_impl(bool utf16, bool count, const uint8_t *inb, uint64_t n_
     const uint8_t *base = inb ? inb - lead : reinterpret_cast<const uint8_t *>(16);
     const uint64_t nchunks = n_tiles(utf16 ? 2 * n_units : n_units, lead, kChunkBytes);
     int rc;
-    if (utf16)
+    if (utf16 && be)
+        rc = launch_validate<true, false, true>(base, lead, n_units, ws, res, nchunks, stream);
+    else if (utf16)
         rc = count ? launch_validate<true, true>(base, lead, n_units, ws, res, nchunks, stream)
                    : launch_validate<true, false>(base, lead, n_units, ws, res, nchunks, stream);
     else
@@ -686,55 +700,9 @@ static int chars_impl(bool utf16, const uint8_t *inb, uint64_t n_units, void *ws
     return 0;
 }
 
-extern "C" {
-
-const char *lu_last_error(void) { return g_err.c_str(); }
-
-#ifdef LU_PROF
-int lu_prof_read(unsigned long long *out32, int reset)
-{
-    cudaError_t e = cudaMemcpyFromSymbol(out32, g_prof, sizeof(g_prof));
-    if (e == cudaSuccess && reset) {
-        static const unsigned long long z[48] = {};
-        e = cudaMemcpyToSymbol(g_prof, z, sizeof(z));
-    }
-    return e == cudaSuccess ? 0 : -1;
-}
-#endif
-
-const char *lu_version(void) { return "laneutf_b200 0.1.0 (sm_100a)"; }
-
-uint64_t lu_workspace_bytes(int op, uint64_t n_units)
-{
-    switch (op) {
-    case LU_OP_UTF8_TO_UTF16LE:
-        return 8 * (n_tiles(n_units, 15, kPipeTile) + 1) + 64;
-    case LU_OP_UTF16LE_TO_UTF8:
-        return 8 * (n_tiles(2 * n_units, 15, kPipeTile) + 1) + 64;
-    case LU_OP_VALIDATE_UTF8:
-    case LU_OP_VALIDATE_UTF16LE:
-    case LU_OP_UTF16_LENGTH_FROM_UTF8:
-    case LU_OP_UTF8_LENGTH_FROM_UTF16LE:
-    case LU_OP_UTF8_CHAR_COUNT:
-    case LU_OP_UTF16LE_CHAR_COUNT:
-        return 64;
-    default:
-        return 0;
-    }
-}
-
-int lu_device_supported(int dev)
-{
-    cudaDeviceProp p;
-    if (cudaGetDeviceProperties(&p, dev) != cudaSuccess)
-        return 0;
-    return p.major == 10 && p.minor == 0;
-}
-
-int lu_tile_bytes(void) { return kPipeTile; }
-
-int lu_utf8_to_utf16le(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint64_t out_cap_words, void *ws,
-                       uint64_t ws_bytes, lu_outcome *res, cudaStream_t stream)
+template <class Dir>
+static int u8u16_impl(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint64_t out_cap_words, void *ws,
+                      uint64_t ws_bytes, lu_outcome *res, cudaStream_t stream)
 {
     if ((!in && n_bytes) || !res || !ws)
         return fail(LU_ERR_INVALID, "null pointer");
@@ -761,10 +729,10 @@ int lu_utf8_to_utf16le(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint6
     const uint32_t out_lead = (uint32_t)(((uintptr_t)out_safe & 15) >> 1);
     uint16_t *out_a = out_safe - out_lead;
     unsigned grid = 0;
-    rc = persistent_grid((const void *)k_transcode<DirU8U16>, kPipeThreads, kSmemK1, nt, &grid, 1);
+    rc = persistent_grid((const void *)k_transcode<Dir>, kPipeThreads, kSmemK1, nt, &grid, 1);
     if (rc)
         return rc;
-    k_transcode<DirU8U16><<<grid, kPipeThreads, kSmemK1, stream>>>(base, lead, n_bytes, n_bytes, out_a, out_lead,
+    k_transcode<Dir><<<grid, kPipeThreads, kSmemK1, stream>>>(base, lead, n_bytes, n_bytes, out_a, out_lead,
                                                                    reinterpret_cast<uint64_t *>(ws),
                                                                    reinterpret_cast<Outcome *>(res), (uint32_t)nt);
     e = cudaGetLastError();
@@ -773,8 +741,9 @@ int lu_utf8_to_utf16le(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint6
     return 0;
 }
 
-int lu_utf16le_to_utf8(const uint16_t *in, uint64_t n_words, uint8_t *out, uint64_t out_cap_bytes, void *ws,
-                       uint64_t ws_bytes, lu_outcome *res, cudaStream_t stream)
+template <class Dir>
+static int u16u8_impl(const uint16_t *in, uint64_t n_words, uint8_t *out, uint64_t out_cap_bytes, void *ws,
+                      uint64_t ws_bytes, lu_outcome *res, cudaStream_t stream)
 {
     if ((!in && n_words) || !res || !ws)
         return fail(LU_ERR_INVALID, "null pointer");
@@ -801,16 +770,90 @@ int lu_utf16le_to_utf8(const uint16_t *in, uint64_t n_words, uint8_t *out, uint6
     uint8_t *out_safe = out ? out : reinterpret_cast<uint8_t *>(16);
     const uint32_t out_lead = (uint32_t)((uintptr_t)out_safe & 15);
     unsigned grid = 0;
-    rc = persistent_grid((const void *)k_transcode<DirU16U8>, kPipeThreads, kSmemK2, nt, &grid, 1);
+    rc = persistent_grid((const void *)k_transcode<Dir>, kPipeThreads, kSmemK2, nt, &grid, 1);
     if (rc)
         return rc;
-    k_transcode<DirU16U8><<<grid, kPipeThreads, kSmemK2, stream>>>(
+    k_transcode<Dir><<<grid, kPipeThreads, kSmemK2, stream>>>(
         base, lead, n_words, 2 * n_words, out_safe - out_lead, out_lead, reinterpret_cast<uint64_t *>(ws),
         reinterpret_cast<Outcome *>(res), (uint32_t)nt);
     e = cudaGetLastError();
     if (e != cudaSuccess)
         return cuda_fail(e, "k_utf16le_to_utf8 launch");
     return 0;
+}
+
+extern "C" {
+
+const char *lu_last_error(void) { return g_err.c_str(); }
+
+#ifdef LU_PROF
+int lu_prof_read(unsigned long long *out32, int reset)
+{
+    cudaError_t e = cudaMemcpyFromSymbol(out32, g_prof, sizeof(g_prof));
+    if (e == cudaSuccess && reset) {
+        static const unsigned long long z[48] = {};
+        e = cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+    }
+    return e == cudaSuccess ? 0 : -1;
+}
+#endif
+
+const char *lu_version(void) { return "laneutf_b200 0.1.0 (sm_100a)"; }
+
+uint64_t lu_workspace_bytes(int op, uint64_t n_units)
+{
+    switch (op) {
+    case LU_OP_UTF8_TO_UTF16LE:
+    case LU_OP_UTF8_TO_UTF16BE:
+        return 8 * (n_tiles(n_units, 15, kPipeTile) + 1) + 64;
+    case LU_OP_UTF16LE_TO_UTF8:
+    case LU_OP_UTF16BE_TO_UTF8:
+        return 8 * (n_tiles(2 * n_units, 15, kPipeTile) + 1) + 64;
+    case LU_OP_VALIDATE_UTF8:
+    case LU_OP_VALIDATE_UTF16LE:
+    case LU_OP_UTF16_LENGTH_FROM_UTF8:
+    case LU_OP_UTF8_LENGTH_FROM_UTF16LE:
+    case LU_OP_UTF8_CHAR_COUNT:
+    case LU_OP_UTF16LE_CHAR_COUNT:
+    case LU_OP_VALIDATE_UTF16BE:
+        return 64;
+    default:
+        return 0;
+    }
+}
+
+int lu_device_supported(int dev)
+{
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, dev) != cudaSuccess)
+        return 0;
+    return p.major == 10 && p.minor == 0;
+}
+
+int lu_tile_bytes(void) { return kPipeTile; }
+
+int lu_utf8_to_utf16le(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint64_t out_cap_words, void *ws,
+                       uint64_t ws_bytes, lu_outcome *res, cudaStream_t stream)
+{
+    return u8u16_impl<DirU8U16>(in, n_bytes, out, out_cap_words, ws, ws_bytes, res, stream);
+}
+
+int lu_utf8_to_utf16be(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint64_t out_cap_words, void *ws,
+                       uint64_t ws_bytes, lu_outcome *res, cudaStream_t stream)
+{
+    return u8u16_impl<DirU8U16T<true>>(in, n_bytes, out, out_cap_words, ws, ws_bytes, res, stream);
+}
+
+int lu_utf16le_to_utf8(const uint16_t *in, uint64_t n_words, uint8_t *out, uint64_t out_cap_bytes, void *ws,
+                       uint64_t ws_bytes, lu_outcome *res, cudaStream_t stream)
+{
+    return u16u8_impl<DirU16U8>(in, n_words, out, out_cap_bytes, ws, ws_bytes, res, stream);
+}
+
+int lu_utf16be_to_utf8(const uint16_t *in, uint64_t n_words, uint8_t *out, uint64_t out_cap_bytes, void *ws,
+                       uint64_t ws_bytes, lu_outcome *res, cudaStream_t stream)
+{
+    return u16u8_impl<DirU16U8T<true>>(in, n_words, out, out_cap_bytes, ws, ws_bytes, res, stream);
 }
 
 int lu_validate_utf8(const uint8_t *in, uint64_t n_bytes, void *ws, uint64_t ws_bytes, lu_outcome *res,
@@ -823,6 +866,12 @@ int lu_validate_utf16le(const uint16_t *in, uint64_t n_words, void *ws, uint64_t
                         cudaStream_t stream)
 {
     return validate_impl(true, false, reinterpret_cast<const uint8_t *>(in), n_words, ws, ws_bytes, res, stream);
+}
+
+int lu_validate_utf16be(const uint16_t *in, uint64_t n_words, void *ws, uint64_t ws_bytes, lu_outcome *res,
+                        cudaStream_t stream)
+{
+    return validate_impl(true, false, reinterpret_cast<const uint8_t *>(in), n_words, ws, ws_bytes, res, stream, true);
 }
 
 int lu_utf16_length_from_utf8(const uint8_t *in, uint64_t n_bytes, void *ws, uint64_t ws_bytes, lu_outcome *res,

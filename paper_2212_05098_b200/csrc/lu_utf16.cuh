@@ -236,7 +236,7 @@ __device__ __forceinline__ void u16_sur_masks(uint32_t x, uint32_t &hs, uint32_t
 // Count = true also returns, in `count`, the UTF-8 length of the chunk's
 // words (1/2/3 bytes per BMP word, 4 per high surrogate, 0 per low one; exact
 // when the input is valid) -- utf8_length_from_utf16le.
-template <bool Boundary, bool Count = false>
+template <bool Boundary, bool Count = false, bool Swap16 = false>
 __device__ __forceinline__ void u16val_warp_r(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
                                               int64_t hi_b, uint32_t &err, uint32_t &err_pos,
                                               uint32_t *count = nullptr)
@@ -245,7 +245,7 @@ __device__ __forceinline__ void u16val_warp_r(const uint8_t *__restrict__ base, 
     const int64_t chunk = tile_off;
     constexpr int kRounds = kChunkBytes / 512;
     ChunkIn in;
-    load_chunk<Boundary>(base, chunk, lo_b, hi_b, in);
+    load_chunk<Boundary, Swap16>(base, chunk, lo_b, hi_b, in);
     const uint4 *q = in.q;
     uint32_t carry = in.halo_p;
     const uint32_t halo_n = in.halo_n;

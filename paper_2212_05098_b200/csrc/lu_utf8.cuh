@@ -324,7 +324,9 @@ __device__ __forceinline__ void sts16_if(uint32_t addr, uint32_t v, uint32_t roo
                  : "memory");
 }
 
-template <bool Boundary>
+// BE: emit UTF-16BE (the word's high byte first): the compaction prmt takes
+// its two byte planes in the other order, at no cost.
+template <bool Boundary, bool BE = false>
 __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
                                            int64_t hi_b, uint16_t *out_w, const SelPair *sel, WarpResult &wr,
                                            uint32_t warp /* warp index inside the tile */, const ChunkIn &in)
@@ -478,8 +480,8 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
             const uint32_t lo = lop[k], hi = hip[k];
             const uint32_t idx = (e[k] * 0x00204081u) >> 28;
             const SelPair sp = sel[idx];
-            const uint32_t w01 = prmt(lo, hi, sp.s01);
-            const uint32_t w23 = prmt(lo, hi, sp.s23);
+            const uint32_t w01 = BE ? prmt(hi, lo, sp.s01) : prmt(lo, hi, sp.s01);
+            const uint32_t w23 = BE ? prmt(hi, lo, sp.s23) : prmt(lo, hi, sp.s23);
             const uint32_t a = sbase + 2 * off;
             const uint32_t room = lane_end - off;
             // Stores past this quad's words are overwritten by the next

@@ -148,6 +148,15 @@ def resolve_engine(engine: EngineKind | str | None = None) -> EngineKind:
     return engine
 
 
+def _check_byte_order(order: str) -> bool:
+    """True for UTF-16BE.  The reference offers BE only through its CLI
+    (swap before / after the LE call, cli.py:90-94, 113-114); here it is a
+    keyword-only extension of the facade, fused into the kernels."""
+    if order not in ("le", "be"):
+        raise ValueError(f"utf16_byte_order must be 'le' or 'be', not {order!r}")
+    return order == "be"
+
+
 def _check_direction(direction: str) -> None:
     if direction not in DIRECTIONS:
         raise ValueError(f"direction must be one of {DIRECTIONS}")
@@ -224,6 +233,7 @@ def transcode_device(
     res: torch.Tensor | None = None,
     ws: torch.Tensor | None = None,
     stream: torch.cuda.Stream | None = None,
+    utf16_byte_order: str = "le",
 ) -> tuple[torch.Tensor, torch.Tensor]:
     """Device-resident transcode, enqueued on ``stream``; no synchronisation.
 
@@ -234,18 +244,19 @@ def transcode_device(
     worst-case output buffer (uint16 words or uint8 bytes).
     """
     _check_direction(direction)
+    be = _check_byte_order(utf16_byte_order)
     device = src.device
     srcb = _to_device_bytes(src, device)
     nbytes = srcb.numel()
     if direction == UTF8_TO_UTF16:
-        op, n_units, cap = _native.OP_UTF8_TO_UTF16LE, nbytes, nbytes
+        op, n_units, cap = (_native.OP_UTF8_TO_UTF16BE if be else _native.OP_UTF8_TO_UTF16LE), nbytes, nbytes
         if out is None:
             out = torch.empty(max(cap, 1), dtype=torch.uint16, device=device)
         out_cap = out.numel() * out.element_size() // 2
     else:
         if nbytes % 2:
             raise ValueError("UTF-16 input must be an even number of bytes")
-        op, n_units = _native.OP_UTF16LE_TO_UTF8, nbytes // 2
+        op, n_units = (_native.OP_UTF16BE_TO_UTF8 if be else _native.OP_UTF16LE_TO_UTF8), nbytes // 2
         cap = 3 * n_units
         if out is None:
             out = torch.empty(max(cap, 1), dtype=torch.uint8, device=device)
@@ -265,9 +276,11 @@ def validate_device(
     res: torch.Tensor | None = None,
     ws: torch.Tensor | None = None,
     stream: torch.cuda.Stream | None = None,
+    utf16_byte_order: str = "le",
 ) -> torch.Tensor:
     """Device-resident validation; returns the int64[3] outcome tensor."""
     _check_direction(direction)
+    be = _check_byte_order(utf16_byte_order)
     device = src.device
     srcb = _to_device_bytes(src, device)
     nbytes = srcb.numel()
@@ -276,7 +289,7 @@ def validate_device(
     else:
         if nbytes % 2:
             raise ValueError("UTF-16 input must be an even number of bytes")
-        op, n_units = _native.OP_VALIDATE_UTF16LE, nbytes // 2
+        op, n_units = (_native.OP_VALIDATE_UTF16BE if be else _native.OP_VALIDATE_UTF16LE), nbytes // 2
     if res is None:
         res = torch.empty(3, dtype=torch.int64, device=device)
     if ws is None:
@@ -315,14 +328,18 @@ def transcode(
     out,
     *,
     engine: EngineKind | str | None = None,
+    utf16_byte_order: str = "le",
 ) -> TranscodeOutcome:
     """Route one transcode call to the B200 engine (engine.py:178-209).
 
     ``consumed`` and ``written`` count code units of the source and
     destination formats.  ``out`` receives exactly the transcoded valid
     prefix (``unit * written`` bytes); nothing past it is touched.
+    ``utf16_byte_order="be"`` (keyword-only extension): the UTF-16 side is
+    big-endian, byte swap fused into the kernels.
     """
     _check_direction(direction)
+    be = _check_byte_order(utf16_byte_order)
     kind = resolve_engine(engine)
     if direction == UTF16_TO_UTF8 and _byte_len(data) % 2:
         raise ValueError("UTF-16 input must be an even number of bytes")
@@ -343,13 +360,13 @@ def transcode(
         cap = src.numel() if direction == UTF8_TO_UTF16 else 3 * (src.numel() // 2)
         if dst.numel() < unit * cap:
             raise ValueError("output buffer smaller than the worst case (worst_case_output_bytes)")
-        return hostpipe.pipelined_transcode(direction == UTF8_TO_UTF16, src, dst)
+        return hostpipe.pipelined_transcode(direction == UTF8_TO_UTF16, src, dst, be=be)
     device = _device()
     src = _to_device_bytes(data, device)
     out_dev = None
     if isinstance(out, torch.Tensor) and out.is_cuda:
         out_dev = out  # kernel writes straight into the caller's device buffer
-    res, buf = transcode_device(direction, src, out_dev)
+    res, buf = transcode_device(direction, src, out_dev, utf16_byte_order=utf16_byte_order)
     outcome = outcome_from_tensor(res.cpu())
     if out_dev is None:
         unit = 2 if direction == UTF8_TO_UTF16 else 1
@@ -363,16 +380,18 @@ def transcode_to_bytes(
     data,
     *,
     engine: EngineKind | str | None = None,
+    utf16_byte_order: str = "le",
 ) -> tuple[TranscodeOutcome, bytes]:
     """Transcode into a fresh worst-case buffer; returns outcome + payload (engine.py:212-223)."""
     _check_direction(direction)
+    _check_byte_order(utf16_byte_order)
     kind = resolve_engine(engine)
     if direction == UTF16_TO_UTF8 and _byte_len(data) % 2:
         raise ValueError("UTF-16 input must be an even number of bytes")
     _require_native(kind)
     device = _device()
     src = _to_device_bytes(data, device)
-    res, buf = transcode_device(direction, src)
+    res, buf = transcode_device(direction, src, utf16_byte_order=utf16_byte_order)
     outcome = outcome_from_tensor(res.cpu())
     unit = 2 if direction == UTF8_TO_UTF16 else 1
     payload = buf.view(torch.uint8)[: unit * outcome.written].cpu().numpy().tobytes()
@@ -384,16 +403,18 @@ def validate(
     data,
     *,
     engine: EngineKind | str | None = None,
+    utf16_byte_order: str = "le",
 ) -> TranscodeOutcome:
     """Validation via the B200 read-only kernels; written is always 0 (engine.py:226-240)."""
     _check_direction(direction)
+    _check_byte_order(utf16_byte_order)
     kind = resolve_engine(engine)
     if direction == UTF16_TO_UTF8 and _byte_len(data) % 2:
         raise ValueError("UTF-16 input must be an even number of bytes")
     _require_native(kind)
     device = _device()
     src = _to_device_bytes(data, device)
-    res = validate_device(direction, src)
+    res = validate_device(direction, src, utf16_byte_order=utf16_byte_order)
     outcome = outcome_from_tensor(res.cpu())
     return TranscodeOutcome(outcome.status, outcome.consumed, 0)
 

@@ -30,11 +30,11 @@ DEFAULT_CHUNK = 64 << 20  # bytes of input per chunk (16 MiB measured slower)
 
 
 def pipelined_transcode(utf8_in: bool, host_in: torch.Tensor, host_out: torch.Tensor,
-                        chunk_bytes: int = DEFAULT_CHUNK) -> TranscodeOutcome:
+                        chunk_bytes: int = DEFAULT_CHUNK, be: bool = False) -> TranscodeOutcome:
     """Transcode pinned ``host_in`` (uint8) into pinned ``host_out`` (uint8).
 
     Writes exactly ``host_out[:unit * written]``.  Returns the whole-buffer
-    outcome.
+    outcome.  ``be``: the UTF-16 side is big-endian.
     """
     dev = torch.device("cuda", torch.cuda.current_device())
     nbytes = host_in.numel()
@@ -44,7 +44,10 @@ def pipelined_transcode(utf8_in: bool, host_in: torch.Tensor, host_out: torch.Te
     units = host_in.view(torch.uint8) if utf8_in else host_in.view(torch.int16)
 
     def unit_at(i: int) -> int:
-        return int(units[i].item()) & 0xFFFF
+        u = int(units[i].item()) & 0xFFFF
+        if be and not utf8_in:
+            u = ((u & 0xFF) << 8) | (u >> 8)
+        return u
 
     step = max(chunk_bytes // unit_in, 1)
     cuts = [0]
@@ -62,7 +65,10 @@ def pipelined_transcode(utf8_in: bool, host_in: torch.Tensor, host_out: torch.Te
     k_chunks = len(cuts) - 1
     res_dev = torch.empty((k_chunks, 3), dtype=torch.int64, device=dev)
     res_host = torch.empty((k_chunks, 3), dtype=torch.int64).pin_memory()
-    op = _native.OP_UTF8_TO_UTF16LE if utf8_in else _native.OP_UTF16LE_TO_UTF8
+    if utf8_in:
+        op = _native.OP_UTF8_TO_UTF16BE if be else _native.OP_UTF8_TO_UTF16LE
+    else:
+        op = _native.OP_UTF16BE_TO_UTF8 if be else _native.OP_UTF16LE_TO_UTF8
 
     s_h2d = torch.cuda.Stream(dev)
     s_comp = torch.cuda.Stream(dev)
