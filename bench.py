@@ -233,6 +233,7 @@ def main():
     from paper_2212_05098_b200 import (
         UTF8_TO_UTF16,
         UTF16_TO_UTF8,
+        batch_device,
         corpus,
         count_device,
         outcome_from_tensor,
@@ -465,6 +466,23 @@ def main():
                         "ok": o.ok}
         extras["row8f_utf16be"] = c9
         del emoji_be
+        # row 8f(3): batched independent cases -- the 2^24 byte-triple sweep
+        tri = torch.arange(1 << 24, dtype=torch.int32, device=dev)
+        tri_data = torch.stack([(tri >> 16) & 255, (tri >> 8) & 255, tri & 255], dim=1).to(torch.uint8).reshape(-1)
+        tri_offs = 3 * torch.arange((1 << 24) + 1, dtype=torch.int64, device=dev)
+        cb = {}
+        for name, vo in (("validate_utf8_all_byte_triples", True), ("utf8_to_utf16_all_byte_triples", False)):
+            batch_device(UTF8_TO_UTF16, tri_data, tri_offs, validate_only=vo)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(3):
+                batch_device(UTF8_TO_UTF16, tri_data, tri_offs, validate_only=vo)
+            b.record(stream)
+            torch.cuda.synchronize()
+            t = a.elapsed_time(b) / 1e3 / 3
+            cb[name] = {"cases": 1 << 24, "ms": round(t * 1e3, 2), "cases_per_s": round((1 << 24) / t)}
+        extras["row8f_batch"] = cb
+        del tri, tri_data, tri_offs
         line["extras"] = extras
 
     if rank == 0 and world == 1:

@@ -24,6 +24,8 @@
  *   lu_utf16le_char_count scalar.utf16le_char_count, scalar.py:251-257
  *   lu_utf8_to_utf16be / lu_utf16be_to_utf8 / lu_validate_utf16be
  *                        the CLI's utf16be formats, cli.py:90-94, 113-114
+ *   lu_batch_*           many independent cases per launch: the difftest
+ *                        campaign / triple sweep, difftest.py:90-104
  *   lu_workspace_bytes   (new) sizing helper; the output sizing rule is
  *                        engine.worst_case_output_bytes, engine.py:171-175
  *   lu_device_supported  engine.detect() capability probe, engine.py:141-153
@@ -127,6 +129,25 @@ int lu_utf8_char_count(const uint8_t *in, uint64_t n_bytes, void *ws, uint64_t w
 
 int lu_utf16le_char_count(const uint16_t *in, uint64_t n_words, void *ws, uint64_t ws_bytes, uint64_t *count,
                           lu_stream_t stream);
+
+/* Batched independent cases (the differential campaign / byte-triple sweep
+ * through the GPU; reference harness difftest.py:90-104):
+ * case i = units [offsets[i], offsets[i+1]) of ``data`` (bytes or 16-bit
+ * words), offsets non-decreasing, n_cases + 1 device uint64 entries.
+ * res[i] = case i's lu_outcome; case i's output is written at its worst-case
+ * slot: out + offsets[i] (words) for UTF-8 -> UTF-16LE, out + 3 * offsets[i]
+ * (bytes) for UTF-16LE -> UTF-8, exactly res[i].written units.  No workspace. */
+int lu_batch_utf8_to_utf16le(const uint8_t *data, const uint64_t *offsets, uint32_t n_cases, uint16_t *out,
+                             lu_outcome *res, lu_stream_t stream);
+
+int lu_batch_utf16le_to_utf8(const uint16_t *data, const uint64_t *offsets, uint32_t n_cases, uint8_t *out,
+                             lu_outcome *res, lu_stream_t stream);
+
+int lu_batch_validate_utf8(const uint8_t *data, const uint64_t *offsets, uint32_t n_cases, lu_outcome *res,
+                           lu_stream_t stream);
+
+int lu_batch_validate_utf16le(const uint16_t *data, const uint64_t *offsets, uint32_t n_cases, lu_outcome *res,
+                              lu_stream_t stream);
 
 uint64_t lu_workspace_bytes(int op, uint64_t n_units);
 

@@ -34,6 +34,7 @@ __all__ = [
     "OP_VALIDATE_UTF16BE",
     "workspace_bytes",
     "launch",
+    "launch_batch",
 ]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblaneutf_b200.so")
@@ -63,6 +64,10 @@ SYMBOLS = (
     "lu_utf8_length_from_utf16le",
     "lu_utf8_char_count",
     "lu_utf16le_char_count",
+    "lu_batch_utf8_to_utf16le",
+    "lu_batch_utf16le_to_utf8",
+    "lu_batch_validate_utf8",
+    "lu_batch_validate_utf16le",
     "lu_workspace_bytes",
     "lu_device_supported",
     "lu_tile_bytes",
@@ -106,6 +111,15 @@ def lib():
                          "lu_utf8_length_from_utf16le", "lu_utf8_char_count", "lu_utf16le_char_count"):
                 fn = getattr(L, name)
                 fn.argtypes = [vp, u64, vp, u64, vp, vp]
+                fn.restype = i32
+            u32 = ctypes.c_uint32
+            for name in ("lu_batch_utf8_to_utf16le", "lu_batch_utf16le_to_utf8"):
+                fn = getattr(L, name)
+                fn.argtypes = [vp, vp, u32, vp, vp, vp]
+                fn.restype = i32
+            for name in ("lu_batch_validate_utf8", "lu_batch_validate_utf16le"):
+                fn = getattr(L, name)
+                fn.argtypes = [vp, vp, u32, vp, vp]
                 fn.restype = i32
             L.lu_workspace_bytes.argtypes = [i32, u64]
             L.lu_workspace_bytes.restype = u64
@@ -155,6 +169,34 @@ def _check(rc: int) -> None:
 
 def _ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
     return ctypes.c_void_p(t.data_ptr() if t is not None and t.numel() else 0)
+
+
+def launch_batch(
+    op: int,
+    data: torch.Tensor,
+    offsets: torch.Tensor,
+    out: torch.Tensor | None,
+    res: torch.Tensor,
+    stream: torch.cuda.Stream | None = None,
+) -> None:
+    """Enqueue one batched call (op in OP_UTF8_TO_UTF16LE, OP_UTF16LE_TO_UTF8,
+    OP_VALIDATE_UTF8, OP_VALIDATE_UTF16LE): ``offsets`` is a CUDA int64 tensor
+    of n_cases + 1 unit offsets into ``data``; ``res`` int64[n_cases, 3]."""
+    L = lib()
+    s = stream if stream is not None else torch.cuda.current_stream(data.device)
+    sp = ctypes.c_void_p(s.cuda_stream)
+    n = offsets.numel() - 1
+    if op == OP_UTF8_TO_UTF16LE:
+        rc = L.lu_batch_utf8_to_utf16le(_ptr(data), _ptr(offsets), n, _ptr(out), _ptr(res), sp)
+    elif op == OP_UTF16LE_TO_UTF8:
+        rc = L.lu_batch_utf16le_to_utf8(_ptr(data), _ptr(offsets), n, _ptr(out), _ptr(res), sp)
+    elif op == OP_VALIDATE_UTF8:
+        rc = L.lu_batch_validate_utf8(_ptr(data), _ptr(offsets), n, _ptr(res), sp)
+    elif op == OP_VALIDATE_UTF16LE:
+        rc = L.lu_batch_validate_utf16le(_ptr(data), _ptr(offsets), n, _ptr(res), sp)
+    else:
+        raise ValueError(f"unknown batch op {op}")
+    _check(rc)
 
 
 def launch(

@@ -487,6 +487,85 @@ __global__ void __launch_bounds__(kThreads) k_validate_w(const uint8_t *__restri
     }
 }
 
+// ================================================================== batched
+//
+// Many small independent cases in one launch (the reference's differential
+// campaign and byte-triple sweep, difftest.py:90-104): case i is
+// units [offs[i], offs[i+1]) of one buffer.  One warp per case walks the
+// case's 2 KiB chunks in order through the same warp bodies as K1-K4
+// (boundary variants, the case bounds as [lo, hi)), carrying its running
+// output count -- no cross-warp ordering, no scanner.  Case i's output goes to
+// its worst-case slot (word offs[i] for UTF-8 -> UTF-16, byte 3 * offs[i] for
+// UTF-16 -> UTF-8); res[i] is its own lu_outcome.
+// Op: 0 utf8 -> utf16le, 1 utf16le -> utf8, 2 validate utf8, 3 validate utf16le.
+template <int Op>
+__global__ void __launch_bounds__(kThreads) k_batch(const uint8_t *__restrict__ base, uint32_t lead,
+                                                    const uint64_t *__restrict__ offs, uint32_t ncases,
+                                                    void *__restrict__ out_a, uint32_t out_lead,
+                                                    Outcome *__restrict__ res)
+{
+    constexpr bool kUtf16 = (Op == 1 || Op == 3);
+    constexpr int kShift = kUtf16 ? 1 : 0;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    __shared__ SelPair sel[16];
+    __shared__ WarpResult wres[kWarps];
+    if (Op == 0)
+        sel_table_init(sel);
+    __syncthreads();
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t lane = lane_id();
+    const uint32_t total_warps = gridDim.x * kWarps;
+    for (uint32_t c = blockIdx.x * kWarps + warp; c < ncases; c += total_warps) {
+        const uint64_t u0 = offs[c], u1 = offs[c + 1];
+        const int64_t lo_b = (int64_t)lead + ((int64_t)u0 << kShift);
+        const int64_t hi_b = (int64_t)lead + ((int64_t)u1 << kShift);
+        uint64_t running = 0, consumed = u1 - u0;
+        uint32_t status = kStatusOk;
+        for (int64_t chunk = lo_b & ~(int64_t)15; chunk < hi_b; chunk += kChunkBytes) {
+            uint32_t err, pos, units = 0;
+            if (Op == 0 || Op == 1) {
+                ChunkIn in;
+                load_chunk<true>(base, chunk, lo_b, hi_b, in);
+                if (Op == 0) {
+                    uint16_t *stage = reinterpret_cast<uint16_t *>(smem_raw) + warp * kOutStrideU16;
+                    u8u16_warp<true>(base, chunk, lo_b, hi_b, stage, sel, wres[warp], 0, in);
+                    __syncwarp();
+                    units = wres[warp].units;
+                    copy_out_u16(stage, units, reinterpret_cast<uint16_t *>(out_a), out_lead + u0 + running);
+                } else {
+                    uint8_t *stage = smem_raw + warp * kOutStrideU8;
+                    u16u8_warp_r<true>(base, chunk, lo_b, hi_b, stage, wres[warp], 0, in);
+                    __syncwarp();
+                    units = wres[warp].units;
+                    copy_out_u8(stage, units, reinterpret_cast<uint8_t *>(out_a), out_lead + 3 * u0 + running);
+                }
+                err = wres[warp].err;
+                pos = wres[warp].pos;
+            } else if (Op == 2) {
+                u8val_warp<true>(base, chunk, lo_b, hi_b, wres[warp], 0);
+                __syncwarp();
+                err = wres[warp].err;
+                pos = wres[warp].pos;
+            } else {
+                u16val_warp_r<true>(base, chunk, lo_b, hi_b, err, pos);
+            }
+            __syncwarp(); // the staging region / result slot is reused next chunk
+            running += units;
+            if (err) {
+                status = kStatusMalformed;
+                consumed = (uint64_t)((chunk + pos - lo_b) >> kShift);
+                break;
+            }
+        }
+        if (lane == 0) {
+            res[c].status = status;
+            res[c].pad = 0;
+            res[c].consumed = consumed;
+            res[c].written = running;
+        }
+    }
+}
+
 // ============================================================ char counts
 //
 // utf8_char_count / utf16le_char_count (scalar.py:246-257): bytes that are
@@ -782,6 +861,51 @@ static int u16u8_impl(const uint16_t *in, uint64_t n_words, uint8_t *out, uint64
     return 0;
 }
 
+template <int Op>
+static int batch_impl(const uint8_t *inb, const uint64_t *offs, uint32_t ncases, void *out, lu_outcome *res,
+                      cudaStream_t stream)
+{
+    constexpr bool kUtf16 = (Op == 1 || Op == 3);
+    if (!offs || (!res && ncases))
+        return fail(LU_ERR_INVALID, "null pointer");
+    if ((kUtf16 && ((uintptr_t)inb & 1)) || ((uintptr_t)offs & 7) || ((uintptr_t)res & 7) ||
+        (Op == 0 && ((uintptr_t)out & 1)))
+        return fail(LU_ERR_INVALID, "misaligned pointer");
+    if ((Op == 0 || Op == 1) && !out && ncases)
+        return fail(LU_ERR_INVALID, "null output");
+    if (ncases == 0)
+        return 0;
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    const size_t smem = Op == 0 ? sizeof(uint16_t) * kOutStrideU16 * kWarps : (Op == 1 ? kOutStrideU8 * kWarps : 0);
+    std::call_once(once, [smem] {
+        attr = cudaFuncSetAttribute(k_batch<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    if (attr != cudaSuccess)
+        return cuda_fail(attr, "cudaFuncSetAttribute");
+    const uint32_t lead = (uint32_t)((uintptr_t)inb & 15);
+    const uint8_t *base = inb ? inb - lead : reinterpret_cast<const uint8_t *>(16);
+    uint32_t out_lead = 0;
+    void *out_a = out;
+    if (Op == 0 && out) {
+        out_lead = (uint32_t)(((uintptr_t)out & 15) >> 1);
+        out_a = reinterpret_cast<uint16_t *>(out) - out_lead;
+    } else if (Op == 1 && out) {
+        out_lead = (uint32_t)((uintptr_t)out & 15);
+        out_a = reinterpret_cast<uint8_t *>(out) - out_lead;
+    }
+    unsigned grid = 0;
+    int rc = persistent_grid((const void *)k_batch<Op>, kThreads, smem, (ncases + kWarps - 1) / kWarps, &grid);
+    if (rc)
+        return rc;
+    k_batch<Op><<<grid, kThreads, smem, stream>>>(base, lead, offs, ncases, out_a, out_lead,
+                                                   reinterpret_cast<Outcome *>(res));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        return cuda_fail(e, "k_batch launch");
+    return 0;
+}
+
 extern "C" {
 
 const char *lu_last_error(void) { return g_err.c_str(); }
@@ -896,6 +1020,30 @@ int lu_utf16le_char_count(const uint16_t *in, uint64_t n_words, void *ws, uint64
                           cudaStream_t stream)
 {
     return chars_impl(true, reinterpret_cast<const uint8_t *>(in), n_words, ws, ws_bytes, count, stream);
+}
+
+int lu_batch_utf8_to_utf16le(const uint8_t *data, const uint64_t *offsets, uint32_t n_cases, uint16_t *out,
+                             lu_outcome *res, cudaStream_t stream)
+{
+    return batch_impl<0>(data, offsets, n_cases, out, res, stream);
+}
+
+int lu_batch_utf16le_to_utf8(const uint16_t *data, const uint64_t *offsets, uint32_t n_cases, uint8_t *out,
+                             lu_outcome *res, cudaStream_t stream)
+{
+    return batch_impl<1>(reinterpret_cast<const uint8_t *>(data), offsets, n_cases, out, res, stream);
+}
+
+int lu_batch_validate_utf8(const uint8_t *data, const uint64_t *offsets, uint32_t n_cases, lu_outcome *res,
+                           cudaStream_t stream)
+{
+    return batch_impl<2>(data, offsets, n_cases, nullptr, res, stream);
+}
+
+int lu_batch_validate_utf16le(const uint16_t *data, const uint64_t *offsets, uint32_t n_cases, lu_outcome *res,
+                              cudaStream_t stream)
+{
+    return batch_impl<3>(reinterpret_cast<const uint8_t *>(data), offsets, n_cases, nullptr, res, stream);
 }
 
 } // extern "C"

@@ -61,6 +61,9 @@ __all__ = [
     "utf8_char_count",
     "utf16le_char_count",
     "count_device",
+    "batch_device",
+    "transcode_batch",
+    "validate_batch",
 ]
 
 UTF8_TO_UTF16 = "utf8-to-utf16"
@@ -473,6 +476,83 @@ def utf16le_char_count(data) -> int:
         raise ValueError("UTF-16 input must be an even number of bytes")
     src = _to_device_bytes(data, _device())
     return int(count_device(_native.OP_UTF16LE_CHAR_COUNT, src).cpu()[0])
+
+
+# ------------------------------------------ batched independent cases (8f)
+
+
+def batch_device(
+    direction: str,
+    data: torch.Tensor,
+    offsets: torch.Tensor,
+    *,
+    validate_only: bool = False,
+    stream: torch.cuda.Stream | None = None,
+) -> tuple[torch.Tensor, torch.Tensor | None]:
+    """Many independent cases in one launch (the difftest campaign / triple
+    sweep through the GPU, SURVEY 8f(3)).  ``data``: CUDA uint8 tensor;
+    ``offsets``: CUDA int64 tensor of n_cases + 1 unit offsets (bytes for
+    UTF-8, 16-bit words for UTF-16).  Returns ``(res, out)``: res int64[n, 3]
+    (status, consumed, written per case) and the output buffer, where case i's
+    payload starts at unit offsets[i] (UTF-8 -> UTF-16, words) or
+    3 * offsets[i] (UTF-16 -> UTF-8, bytes).  No synchronisation."""
+    _check_direction(direction)
+    srcb = _to_device_bytes(data, data.device)
+    n = offsets.numel() - 1
+    res = torch.empty((max(n, 1), 3), dtype=torch.int64, device=srcb.device)
+    out = None
+    if direction == UTF8_TO_UTF16:
+        op = _native.OP_VALIDATE_UTF8 if validate_only else _native.OP_UTF8_TO_UTF16LE
+        if not validate_only:
+            out = torch.empty(max(srcb.numel(), 1), dtype=torch.uint16, device=srcb.device)
+    else:
+        if srcb.numel() % 2:
+            raise ValueError("UTF-16 input must be an even number of bytes")
+        op = _native.OP_VALIDATE_UTF16LE if validate_only else _native.OP_UTF16LE_TO_UTF8
+        if not validate_only:
+            out = torch.empty(max(3 * (srcb.numel() // 2), 1), dtype=torch.uint8, device=srcb.device)
+    if n > 0:
+        _native.launch_batch(op, srcb, offsets, out, res, stream)
+    return res[:n], out
+
+
+def _pack_cases(direction: str, cases) -> tuple[torch.Tensor, torch.Tensor]:
+    unit = 1 if direction == UTF8_TO_UTF16 else 2
+    lens = [len(c) for c in cases]
+    if unit == 2 and any(n % 2 for n in lens):
+        raise ValueError("UTF-16 input must be an even number of bytes")
+    offs = np.zeros(len(cases) + 1, dtype=np.int64)
+    np.cumsum(np.asarray(lens, dtype=np.int64) // unit, out=offs[1:])
+    blob = b"".join(bytes(c) for c in cases)
+    dev = _device()
+    return _to_device_bytes(blob, dev), torch.from_numpy(offs).to(dev)
+
+
+def transcode_batch(direction: str, cases) -> list[tuple[TranscodeOutcome, bytes]]:
+    """``transcode_to_bytes`` for every case of a list, in one launch."""
+    data, offs = _pack_cases(direction, cases)
+    res, out = batch_device(direction, data, offs)
+    rows = res.cpu().tolist()
+    offs_h = offs.cpu().tolist()
+    outb = out.view(torch.uint8).cpu().numpy() if out is not None else None
+    result = []
+    for i, (st, consumed, written) in enumerate(rows):
+        o = TranscodeOutcome(STATUS_BY_CODE[st & 0xFFFFFFFF], consumed, written)
+        if direction == UTF8_TO_UTF16:
+            a = 2 * offs_h[i]
+            payload = outb[a: a + 2 * written].tobytes()
+        else:
+            a = 3 * offs_h[i]
+            payload = outb[a: a + written].tobytes()
+        result.append((o, payload))
+    return result
+
+
+def validate_batch(direction: str, cases) -> list[TranscodeOutcome]:
+    """``validate`` for every case of a list, in one launch."""
+    data, offs = _pack_cases(direction, cases)
+    res, _ = batch_device(direction, data, offs, validate_only=True)
+    return [TranscodeOutcome(STATUS_BY_CODE[st & 0xFFFFFFFF], c, 0) for st, c, _ in res.cpu().tolist()]
 
 
 def swap_utf16_byte_order(data: bytes) -> bytes:
