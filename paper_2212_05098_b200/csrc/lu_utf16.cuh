@@ -65,6 +65,11 @@ __device__ __forceinline__ uint32_t valid_words(int64_t a, int64_t lo, int64_t h
     return (uint32_t)(a >= lo && a + 2 <= hi) | ((uint32_t)(a + 2 >= lo && a + 4 <= hi) << 1);
 }
 
+__device__ __forceinline__ void sts8(uint32_t addr, uint32_t v)
+{
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void sts8_if(uint32_t addr, uint32_t v, uint32_t n, uint32_t j)
 {
     asm volatile("{\n\t.reg .pred p;\n\tsetp.gt.u32 p, %2, %3;\n\t@p st.shared.u8 [%0], %1;\n\t}" ::"r"(addr),
@@ -113,6 +118,56 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
             any |= u16_any_sur(w[k]) ? 1u : 0u;
         any |= is_ls(w[5] & 0xFFFFu) ? 1u : 0u;
         const bool sur = __any_sync(0xffffffffu, any != 0);
+        // path A (warp-uniform, interior chunks): no surrogate and every word
+        // < U+0800, so each word is 1 or 2 bytes -- both words of a quad are
+        // encoded in SWAR and packed into one 32-bit byte string
+        bool path_a = false;
+        if (!Boundary && !sur) {
+            uint32_t any800 = 0;
+#pragma unroll
+            for (int k = 1; k <= 4; ++k)
+                any800 |= w[k] & 0xF800F800u;
+            path_a = !__any_sync(0xffffffffu, any800 != 0);
+        }
+        if (path_a) {
+            // self-contained (own scan and stores): its live ranges do not
+            // overlap the general path's, which otherwise spills
+            uint32_t pk[4], nb[4], cnt = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t x = w[k + 1];
+                const uint32_t a = x & 0xFF80FF80u;
+                const uint32_t big = (((a & 0x7FFF7FFFu) + 0x7FFF7FFFu) | a) & 0x80008000u; // word >= 0x80
+                // both halves as 2-byte forms: 110xxxxx 10xxxxxx
+                const uint32_t e2 = ((x >> 6) & 0x001F001Fu) | ((x << 8) & 0x3F003F00u) | 0x80C080C0u;
+                const uint32_t m = prmt(big, 0u, 0xBB99u); // 0xFFFF in each half with a 2-byte word
+                const uint32_t v = (e2 & m) | (x & ~m);     // per half: its 1 or 2 bytes
+                // pack: drop the empty high byte of a 1-byte low word
+                pk[k] = prmt(v, v, (big & 0x8000u) ? 0x3210u : 0x3320u);
+                nb[k] = 2u + (big >> 15 & 1u) + (big >> 31);
+                cnt += nb[k];
+            }
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= (uint32_t)d)
+                    incl += o;
+            }
+            uint32_t off = running + incl - cnt;
+            // 2..4 bytes per quad: two unconditional, two predicated stores
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t a = sbase + off;
+                sts8(a, pk[k]);
+                sts8(a + 1, pk[k] >> 8);
+                sts8_if(a + 2, pk[k] >> 16, nb[k], 2);
+                sts8_if(a + 3, pk[k] >> 24, nb[k], 3);
+                off += nb[k];
+            }
+            running += __shfl_sync(0xffffffffu, incl, 31);
+            continue;
+        }
         uint32_t lo[4], hi[4], n[4], bad[4];
         uint32_t cnt = 0, anybad = 0;
 #pragma unroll
