@@ -121,13 +121,68 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
         // path A (warp-uniform, interior chunks): no surrogate and every word
         // < U+0800, so each word is 1 or 2 bytes -- both words of a quad are
         // encoded in SWAR and packed into one 32-bit byte string
-        bool path_a = false;
+        bool path_a = false, path_b = false;
         if (!Boundary && !sur) {
             uint32_t any800 = 0;
 #pragma unroll
             for (int k = 1; k <= 4; ++k)
                 any800 |= w[k] & 0xF800F800u;
             path_a = !__any_sync(0xffffffffu, any800 != 0);
+            if (!path_a) {
+                // path B: no 2-byte word (every word ASCII or >= U+0800)
+                uint32_t two = 0;
+#pragma unroll
+                for (int k = 1; k <= 4; ++k) {
+                    const uint32_t a = w[k] & 0x07800780u, b = w[k] & 0xF800F800u;
+                    const uint32_t nza = ((a & 0x7FFF7FFFu) + 0x7FFF7FFFu) | a;
+                    const uint32_t nzb = ((b & 0x7FFF7FFFu) + 0x7FFF7FFFu) | b;
+                    two |= nza & ~nzb;
+                }
+                path_b = !__any_sync(0xffffffffu, (two & 0x80008000u) != 0);
+            }
+        }
+        if (path_b) {
+            // both words of a quad as 1 or 3 bytes: three SWAR byte planes,
+            // packed into (lo, hi) with two prmt; 2, 4 or 6 bytes per quad
+            uint32_t pl[4], ph[4], nb[4], cnt = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t x = w[k + 1];
+                const uint32_t a = x & 0xFF80FF80u;
+                const uint32_t big = (((a & 0x7FFF7FFFu) + 0x7FFF7FFFu) | a) & 0x80008000u; // 3-byte word
+                const uint32_t m = prmt(big, 0u, 0xBB99u);
+                const uint32_t b0 = ((x >> 12) & 0x000F000Fu) | 0x00E000E0u; // 1110xxxx
+                const uint32_t b1 = ((x >> 6) & 0x003F003Fu) | 0x00800080u;  // 10xxxxxx
+                const uint32_t b2 = (x & 0x003F003Fu) | 0x00800080u;         // 10xxxxxx
+                const uint32_t av = (b0 & m) | (x & ~m);                     // first byte of each word
+                const uint32_t pp = prmt(av, b1, 0x6240u);                   // [A0, B1_0, A1, B1_1]
+                // word 0 three bytes: [A0 B1_0 B2_0 A1 | B1_1 B2_1]; else [A0 A1 B1_1 B2_1]
+                pl[k] = prmt(pp, b2, (big & 0x8000u) ? 0x2410u : 0x6320u);
+                ph[k] = prmt(pp, b2, 0x0063u);
+                nb[k] = 2u + 2u * ((big >> 15 & 1u) + (big >> 31));
+                cnt += nb[k];
+            }
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= (uint32_t)d)
+                    incl += o;
+            }
+            uint32_t off = running + incl - cnt;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t a = sbase + off;
+                sts8(a, pl[k]);
+                sts8(a + 1, pl[k] >> 8);
+                sts8_if(a + 2, pl[k] >> 16, nb[k], 2);
+                sts8_if(a + 3, pl[k] >> 24, nb[k], 3);
+                sts8_if(a + 4, ph[k], nb[k], 4);
+                sts8_if(a + 5, ph[k] >> 8, nb[k], 5);
+                off += nb[k];
+            }
+            running += __shfl_sync(0xffffffffu, incl, 31);
+            continue;
         }
         if (path_a) {
             // self-contained (own scan and stores): its live ranges do not
