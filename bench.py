@@ -483,6 +483,28 @@ def main():
             cb[name] = {"cases": 1 << 24, "ms": round(t * 1e3, 2), "cases_per_s": round((1 << 24) / t)}
         extras["row8f_batch"] = cb
         del tri, tri_data, tri_offs
+        # config 5 on one GPU: 16 GiB of mixed-profile 64 MiB segments each way
+        if world == 1:
+            c5 = {}
+            for name, utf16 in (("utf8_to_utf16_16GiB", False), ("utf16_to_utf8_16GiB", True)):
+                units = (16 << 30) // (2 if utf16 else 1)
+                big = corpus.config5_generate(units, utf16=utf16, device=dev)
+                direction = UTF16_TO_UTF8 if utf16 else UTF8_TO_UTF16
+                res, bout = transcode_device(direction, big)
+                o = outcome_from_tensor(res.cpu())
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(3):
+                    transcode_device(direction, big, bout, res=res)
+                b.record(stream)
+                torch.cuda.synchronize()
+                t = a.elapsed_time(b) / 1e3 / 3
+                ab = (16 << 30) + (1 if utf16 else 2) * o.written
+                c5[name] = {"input_gib_s": round(16 / t, 2), "frac_of_measured": round(ab / t / 1e9 / peak, 4),
+                            "ok": o.ok, "written": o.written}
+                del big, bout, res
+                torch.cuda.empty_cache()
+            extras["config5_single_gpu"] = c5
         line["extras"] = extras
 
     if rank == 0 and world == 1:

@@ -36,6 +36,7 @@ __all__ = [
     "UTF8_ERROR_KINDS",
     "UTF16_ERROR_KINDS",
     "config5_segments",
+    "config5_generate",
 ]
 
 GOLDEN = 0x9E3779B97F4A7C15
@@ -333,4 +334,19 @@ def config5_segments(total_units: int, seed: int = 5, segment_units: int = 64 <<
     for k in range(n):
         units = min(seg, total_units - k * seg)
         out.append((names[int(_below(draws[k].view(1), 4)[0])], 1000 * seed + k, units))
+    return out
+
+
+def config5_generate(total_units: int, *, seed: int = 5, utf16: bool = False, device="cuda",
+                     segment_units: int = 64 << 20) -> torch.Tensor:
+    """Config 5 buffer (the concatenated seeded 64 MiB segments of
+    ``config5_segments``), generated segment by segment on ``device``; uint8
+    (UTF-8 bytes, or UTF-16LE words as 2 * total_units bytes).  Segments end
+    on character boundaries, so the buffer is valid text."""
+    unit = 2 if utf16 else 1
+    out = torch.empty(unit * total_units, dtype=torch.uint8, device=device)
+    pos = 0
+    for name, sseed, units in config5_segments(total_units, seed, segment_units, utf16):
+        out[unit * pos: unit * (pos + units)] = generate(name, units, sseed, utf16=utf16, device=device)
+        pos += units
     return out

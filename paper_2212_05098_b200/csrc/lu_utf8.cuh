@@ -177,15 +177,13 @@ __device__ __forceinline__ void u8_round_detect(U8Round &R)
         R.det = det;
         return;
     }
-    uint32_t anyf = 0, any2 = 0, any3 = 0;
+    uint32_t anyf = 0, any2 = 0;
 #pragma unroll
     for (int k = 0; k <= 4; ++k) {
         R.m[k].F = R.m[k].E & (R.w[k] << 3);
         anyf |= R.m[k].F;
-        if (k > 0) {
+        if (k > 0)
             any2 |= R.m[k].L & ~R.m[k].E;
-            any3 |= R.m[k].E & ~R.m[k].F;
-        }
     }
     if (!__any_sync(0xffffffffu, (anyf | any2) != 0)) {
         R.path = 1;
@@ -204,6 +202,10 @@ __device__ __forceinline__ void u8_round_detect(U8Round &R)
         R.det = det;
         return;
     }
+    uint32_t any3 = 0; // 3-byte leads (only needed once path 1 is ruled out)
+#pragma unroll
+    for (int k = 1; k <= 4; ++k)
+        any3 |= R.m[k].E & ~R.m[k].F;
     if (!__any_sync(0xffffffffu, (any2 | any3) != 0)) {
         R.path = 3;
 #pragma unroll

@@ -398,3 +398,54 @@ def test_kernels_on_pinned_host_buffers(cuda_ok, utf16):
             assert res_h.cpu().tolist() == res_d.cpu().tolist()
         w = int(res_d[2]) * (1 if utf16 else 2)
         assert torch.equal(h_out[:w], d_out[:w].cpu())
+
+
+# ------------------------------------------------ config 5 (16 GiB, sharded)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("utf16", [False, True])
+def test_config5_full_size_single_gpu(cuda_ok, utf16):
+    """16 GiB of config-5 text (mixed profiles in seeded 64 MiB segments) on
+    one GPU: the UTF-8 <-> UTF-16 round trip is exact, and cutting the input
+    at character boundaries into P = 2, 4, 8 shards, transcoding each shard
+    separately and combining the per-shard records (the multi-GPU rule,
+    shard.combine_records) reproduces the whole-buffer outcome and output."""
+    from paper_2212_05098_b200 import shard
+
+    dev = torch.device("cuda", 0)
+    units = (16 << 30) // (2 if utf16 else 1)
+    src = corpus.config5_generate(units, utf16=utf16, device=dev)
+    direction = UTF16_TO_UTF8 if utf16 else UTF8_TO_UTF16
+    back_dir = UTF8_TO_UTF16 if utf16 else UTF16_TO_UTF8
+    res, out = transcode_device(direction, src)
+    whole = outcome_from_tensor(res.cpu())
+    assert whole.ok and whole.consumed == units
+    unit_out = 1 if utf16 else 2
+    payload = out.view(torch.uint8)[: unit_out * whole.written]
+    res2, back = transcode_device(back_dir, payload)
+    o2 = outcome_from_tensor(res2.cpu())
+    assert o2.ok and torch.equal(back.view(torch.uint8)[: src.numel()], src)
+    del back, res2
+    words = src.view(torch.int16) if utf16 else src
+
+    def unit_at(i):
+        return int(words[i].item()) & 0xFFFF
+
+    for world in (2, 4, 8):
+        cuts = shard.plan_cuts(units, world, unit_at, utf16)
+        records = []
+        off = 0
+        for r in range(world):
+            a, b = cuts[r], cuts[r + 1]
+            piece = src[a * (2 if utf16 else 1): b * (2 if utf16 else 1)]
+            rr, oo = transcode_device(direction, piece)
+            rec = outcome_from_tensor(rr.cpu())
+            records.append((0 if rec.ok else 1, rec.consumed, rec.written))
+            # the shard's payload is the whole payload's slice at its offset
+            got = oo.view(torch.uint8)[: unit_out * rec.written]
+            assert torch.equal(got, payload[unit_out * off: unit_out * (off + rec.written)])
+            off += rec.written
+            del rr, oo, got
+        status, consumed, written, offsets = shard.combine_records(records, cuts[:-1])
+        assert (status, consumed, written) == (0, units, whole.written)
