@@ -60,8 +60,7 @@ __device__ __forceinline__ void copy_out_u16(const uint16_t *src, uint32_t cnt, 
             const uint32_t v = c - 1;                                                                                  \
             const uint4 a = s128[v], b = s128[v + 1];                                                                  \
             const uint32_t w0 = a.x, w1 = a.y, w2 = a.z, w3 = a.w, w4 = b.x, w5 = b.y, w6 = b.z, w7 = b.w;             \
-            (void)w0;                                                                                                  \
-            (void)w7;                                                                                                  \
+            (void)w0, (void)w1, (void)w2, (void)w3, (void)w4, (void)w5, (void)w6, (void)w7;                            \
             __stcs(d128 + c, BODY);                                                                                    \
         }                                                                                                              \
         break;
