@@ -38,10 +38,15 @@ def short(name: str) -> str:
         return "K1 utf8->utf16 (k_transcode<DirU8U16>)"
     if "DirU16U8" in name or "utf16le_to_utf8" in name:
         return "K2 utf16->utf8"
-    if "k_validate<(bool)0>" in name or "k_validate<0>" in name or name.endswith("k_validate<false>"):
-        return "K3 validate utf8"
     if "k_validate" in name:
-        return "K4 validate utf16" if ("1>" in name or "true" in name) else "K3 validate utf8"
+        # first template flag: Utf16 (k_validate_w<Utf16, Count, Swap16>)
+        flags = name.split("<", 1)[1] if "<" in name else ""
+        first = flags.split(",")[0].strip(" >")
+        return "K4 validate utf16" if first in ("1", "true", "(bool)1") else "K3 validate utf8"
+    if "k_chars" in name:
+        return "char count"
+    if "k_batch" in name:
+        return "batch"
     return name.strip()
 
 
