@@ -329,13 +329,14 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
 // (resp. low) surrogate.
 __device__ __forceinline__ void u16_sur_masks(uint32_t x, uint32_t &hs, uint32_t &ls)
 {
-    const uint32_t a = (x & 0xFC00FC00u) ^ 0xD800D800u; // 0 for a high surrogate, 0x0400 for a low one
-    const uint32_t b = a ^ 0x04000400u;
-    // bit 15 of each half set iff that half is nonzero (exact; no carry between halves)
-    const uint32_t nza = ((a & 0x7FFF7FFFu) + 0x7FFF7FFFu) | a;
-    const uint32_t nzb = ((b & 0x7FFF7FFFu) + 0x7FFF7FFFu) | b;
-    hs = ~nza & 0x80008000u;
-    ls = ~nzb & 0x80008000u;
+    // one zero test for "surrogate" ((w & 0xF800) == 0xD800, exact per half:
+    // no carry between halves), then bit 10 (moved to bit 15) splits high
+    // from low
+    const uint32_t c = (x & 0xF800F800u) ^ 0xD800D800u;
+    const uint32_t sur = ~(((c & 0x7FFF7FFFu) + 0x7FFF7FFFu) | c) & 0x80008000u;
+    const uint32_t lowbit = x << 5; // bit 10 -> 15, bit 26 -> 31
+    hs = sur & ~lowbit;
+    ls = sur & lowbit;
 }
 
 // K4 warp body: validate one 2 KiB chunk (1024 words) in 4 rounds of 512 B,
