@@ -65,6 +65,20 @@ __device__ __forceinline__ uint32_t valid_words(int64_t a, int64_t lo, int64_t h
     return (uint32_t)(a >= lo && a + 2 <= hi) | ((uint32_t)(a + 2 >= lo && a + 4 <= hi) << 1);
 }
 
+// SWAR surrogate masks of a quad (two words): bit 15 / 31 set for a high
+// (resp. low) surrogate.
+__device__ __forceinline__ void u16_sur_masks(uint32_t x, uint32_t &hs, uint32_t &ls)
+{
+    // one zero test for "surrogate" ((w & 0xF800) == 0xD800, exact per half:
+    // no carry between halves), then bit 10 (moved to bit 15) splits high
+    // from low
+    const uint32_t c = (x & 0xF800F800u) ^ 0xD800D800u;
+    const uint32_t sur = ~(((c & 0x7FFF7FFFu) + 0x7FFF7FFFu) | c) & 0x80008000u;
+    const uint32_t lowbit = x << 5; // bit 10 -> 15, bit 26 -> 31
+    hs = sur & ~lowbit;
+    ls = sur & lowbit;
+}
+
 __device__ __forceinline__ void sts8(uint32_t addr, uint32_t v)
 {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -118,6 +132,73 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
             any |= u16_any_sur(w[k]) ? 1u : 0u;
         any |= is_ls(w[5] & 0xFFFFu) ? 1u : 0u;
         const bool sur = __any_sync(0xffffffffu, any != 0);
+        // path C (warp-uniform, interior chunks): surrogates present, but every
+        // word is ASCII or a surrogate and every pair is well formed (so no
+        // error): a quad is at most 5 bytes -- the 4-byte forms of both
+        // halves come from SWAR byte planes, then two byte-string selects
+        if (!Boundary && sur) {
+            uint32_t hs[6], ls[6], other = 0;
+#pragma unroll
+            for (int k = 0; k < 6; ++k)
+                u16_sur_masks(w[k], hs[k], ls[k]);
+            uint32_t det = 0;
+#pragma unroll
+            for (int k = 1; k <= 4; ++k) {
+                const uint32_t a = w[k] & 0xFF80FF80u;
+                const uint32_t big = (((a & 0x7FFF7FFFu) + 0x7FFF7FFFu) | a) & 0x80008000u;
+                other |= big & ~(hs[k] | ls[k]); // a BMP word >= 0x80
+            }
+#pragma unroll
+            for (int k = 1; k <= 5; ++k)
+                det |= ls[k] ^ fsl(hs[k - 1], hs[k], 16);
+            if (!__any_sync(0xffffffffu, (other | det) != 0)) {
+                uint32_t pl[4], ph[4], nb[4], cnt = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t x = w[k + 1];
+                    const uint32_t nx = fsr(x, w[k + 2], 16); // the word after each half
+                    const uint32_t U = (x & 0x03FF03FFu) + 0x00400040u;  // cp >> 10 of a pair led by each half
+                    const uint32_t L = nx & 0x03FF03FFu;                  // low 10 bits of the pair
+                    const uint32_t b0 = ((U >> 8) & 0x00070007u) | 0x00F000F0u;
+                    const uint32_t b1 = ((U >> 2) & 0x003F003Fu) | 0x00800080u;
+                    const uint32_t b2 = ((U << 4) & 0x00300030u) | ((L >> 6) & 0x000F000Fu) | 0x00800080u;
+                    const uint32_t b3 = (L & 0x003F003Fu) | 0x00800080u;
+                    const uint32_t p01 = prmt(b0, b1, 0x6240u), p23 = prmt(b2, b3, 0x6240u);
+                    const uint32_t e0 = prmt(p01, p23, 0x5410u), e1 = prmt(p01, p23, 0x7632u);
+                    const bool h0 = hs[k + 1] & 0x8000u, h1 = hs[k + 1] >> 31;
+                    const bool l0 = ls[k + 1] & 0x8000u, l1 = ls[k + 1] >> 31;
+                    const uint32_t t0 = h0 ? e0 : (x & 0xFFu);
+                    const uint32_t t1 = h1 ? e1 : ((x >> 16) & 0xFFu);
+                    const uint32_t n0 = h0 ? 4u : (l0 ? 0u : 1u);
+                    const uint32_t n1 = h1 ? 4u : (l1 ? 0u : 1u);
+                    pl[k] = n0 == 4u ? t0 : (n0 == 1u ? ((t0 & 0xFFu) | (t1 << 8)) : t1);
+                    ph[k] = n0 == 4u ? t1 : (n0 == 1u ? (t1 >> 24) : 0u);
+                    nb[k] = n0 + n1;
+                    cnt += nb[k];
+                }
+                uint32_t incl = cnt;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= (uint32_t)d)
+                        incl += o;
+                }
+                uint32_t off = running + incl - cnt;
+                // 1..5 bytes per quad (valid pairs: AA 2, AH 5, HL 4, LA 1, LH 4)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t a = sbase + off;
+                    sts8(a, pl[k]);
+                    sts8_if(a + 1, pl[k] >> 8, nb[k], 1);
+                    sts8_if(a + 2, pl[k] >> 16, nb[k], 2);
+                    sts8_if(a + 3, pl[k] >> 24, nb[k], 3);
+                    sts8_if(a + 4, ph[k], nb[k], 4);
+                    off += nb[k];
+                }
+                running += __shfl_sync(0xffffffffu, incl, 31);
+                continue;
+            }
+        }
         // path A (warp-uniform, interior chunks): no surrogate and every word
         // < U+0800, so each word is 1 or 2 bytes -- both words of a quad are
         // encoded in SWAR and packed into one 32-bit byte string
@@ -325,19 +406,6 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
     }
 }
 
-// SWAR surrogate masks of a quad (two words): bit 15 / 31 set for a high
-// (resp. low) surrogate.
-__device__ __forceinline__ void u16_sur_masks(uint32_t x, uint32_t &hs, uint32_t &ls)
-{
-    // one zero test for "surrogate" ((w & 0xF800) == 0xD800, exact per half:
-    // no carry between halves), then bit 10 (moved to bit 15) splits high
-    // from low
-    const uint32_t c = (x & 0xF800F800u) ^ 0xD800D800u;
-    const uint32_t sur = ~(((c & 0x7FFF7FFFu) + 0x7FFF7FFFu) | c) & 0x80008000u;
-    const uint32_t lowbit = x << 5; // bit 10 -> 15, bit 26 -> 31
-    hs = sur & ~lowbit;
-    ls = sur & lowbit;
-}
 
 // K4 warp body: validate one 2 KiB chunk (1024 words) in 4 rounds of 512 B,
 // lane l holding words [8l, 8l+8) in registers.  A low surrogate must sit
