@@ -225,6 +225,44 @@ def test_canary_no_write_past_written(cuda_ok):
     assert set(buf[2 * got.written :]) == {0xEE}
 
 
+@pytest.mark.parametrize("utf16", [False, True])
+@pytest.mark.parametrize("be", [False, True])
+def test_guard_bytes_around_misaligned_outputs(cuda_ok, utf16, be):
+    """Output placed at every misaligned device offset inside a guarded
+    buffer: bytes before the output and past ``written`` keep their guard
+    value (own bounds check in place of a sanitizer), for valid and malformed
+    inputs, LE and BE."""
+    from paper_2212_05098_b200 import swap_utf16_byte_order
+
+    dev = torch.device("cuda", 0)
+    unit_out = 1 if utf16 else 2
+    base = corpus.generate("emoji" if utf16 else "mix", 3 * TILE // (2 if utf16 else 1) + 77, seed=25,
+                           utf16=utf16).numpy().view(np.uint8)
+    for err_at in (None, 2 * 700, 2 * (TILE // 2 + 5)):
+        data = base.copy()
+        if err_at is not None:
+            data[err_at: err_at + 2] = [0x00, 0xDC] if utf16 else [0xC1, 0x80]
+        ref, ref_payload = (oracle.utf16le_to_utf8 if utf16 else oracle.utf8_to_utf16le)(data.tobytes())
+        src_bytes = swap_utf16_byte_order(data.tobytes()) if (utf16 and be) else data.tobytes()
+        if be and not utf16:
+            ref_payload = swap_utf16_byte_order(ref_payload)
+        src = torch.frombuffer(bytearray(src_bytes), dtype=torch.uint8).to(dev)
+        cap = 3 * (len(data) // 2) if utf16 else 2 * len(data)
+        for shift in range(0, 16, 1 if utf16 else 2):
+            guard = torch.full((cap + 64,), 0x5A, dtype=torch.uint8, device=dev)
+            out = guard[16 + shift: 16 + shift + cap]
+            direction = UTF16_TO_UTF8 if utf16 else UTF8_TO_UTF16
+            res, _ = transcode_device(direction, src, out if utf16 else out.view(torch.uint16),
+                                      utf16_byte_order="be" if be else "le")
+            got = outcome_from_tensor(res.cpu())
+            assert got.as_tuple() == ref, (shift, err_at)
+            host = guard.cpu().numpy()
+            w = unit_out * got.written
+            assert (host[: 16 + shift] == 0x5A).all(), ("before", shift, err_at)
+            assert host[16 + shift: 16 + shift + w].tobytes() == ref_payload, (shift, err_at)
+            assert (host[16 + shift + w:] == 0x5A).all(), ("after", shift, err_at)
+
+
 # ------------------------------------------------------ full-size configs
 
 
