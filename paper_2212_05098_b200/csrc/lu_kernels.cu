@@ -646,27 +646,38 @@ static uint64_t n_tiles(uint64_t bytes, uint32_t lead, uint64_t tile = kTileByte
     return t ? t : 1;
 }
 
+// cudaFuncSetAttribute is per device: remember, per device, which kernels
+// already have their dynamic shared memory limit raised (a process may drive
+// several GPUs).  Bit k of g_attr_done[dev] = attribute group k is set.
+static std::mutex g_attr_mu;
+static uint64_t g_attr_done[64];
+
+static int ensure_smem_attr(int group, const void *const *fns, const int *bytes, int nfns)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "cudaGetDevice");
+    if (dev < 0 || dev >= 64)
+        return fail(LU_ERR_INVALID, "device index out of range");
+    std::lock_guard<std::mutex> lock(g_attr_mu);
+    if (g_attr_done[dev] & (1ull << group))
+        return 0;
+    for (int k = 0; k < nfns; ++k) {
+        e = cudaFuncSetAttribute(fns[k], cudaFuncAttributeMaxDynamicSharedMemorySize, bytes[k]);
+        if (e != cudaSuccess)
+            return cuda_fail(e, "cudaFuncSetAttribute");
+    }
+    g_attr_done[dev] |= 1ull << group;
+    return 0;
+}
+
 static int set_smem_attrs()
 {
-    static std::once_flag once;
-    static cudaError_t status = cudaSuccess;
-    std::call_once(once, [] {
-        cudaError_t e;
-        e = cudaFuncSetAttribute(k_transcode<DirU8U16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemK1);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_transcode<DirU16U8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kSmemK2);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_transcode<DirU8U16T<true>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kSmemK1);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_transcode<DirU16U8T<true>>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kSmemK2);
-        status = e;
-    });
-    if (status != cudaSuccess)
-        return cuda_fail(status, "cudaFuncSetAttribute");
-    return 0;
+    const void *fns[4] = {(const void *)k_transcode<DirU8U16>, (const void *)k_transcode<DirU16U8>,
+                          (const void *)k_transcode<DirU8U16T<true>>, (const void *)k_transcode<DirU16U8T<true>>};
+    const int bytes[4] = {(int)kSmemK1, (int)kSmemK2, (int)kSmemK1, (int)kSmemK2};
+    return ensure_smem_attr(0, fns, bytes, 4);
 }
 
 // Grid of a persistent pipelined kernel: every CTA must be resident (tiles
@@ -874,14 +885,11 @@ static int batch_impl(const uint8_t *inb, const uint64_t *offs, uint32_t ncases,
         return fail(LU_ERR_INVALID, "null output");
     if (ncases == 0)
         return 0;
-    static std::once_flag once;
-    static cudaError_t attr = cudaSuccess;
     const size_t smem = Op == 0 ? sizeof(uint16_t) * kOutStrideU16 * kWarps : (Op == 1 ? kOutStrideU8 * kWarps : 0);
-    std::call_once(once, [smem] {
-        attr = cudaFuncSetAttribute(k_batch<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    });
-    if (attr != cudaSuccess)
-        return cuda_fail(attr, "cudaFuncSetAttribute");
+    const void *fn = (const void *)k_batch<Op>;
+    const int sb = (int)smem;
+    if (int rc = ensure_smem_attr(1 + Op, &fn, &sb, 1))
+        return rc;
     const uint32_t lead = (uint32_t)((uintptr_t)inb & 15);
     const uint8_t *base = inb ? inb - lead : reinterpret_cast<const uint8_t *>(16);
     uint32_t out_lead = 0;
