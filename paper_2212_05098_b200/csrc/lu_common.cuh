@@ -63,6 +63,20 @@ __device__ __forceinline__ uint32_t fsr(uint32_t lo, uint32_t hi, uint32_t s)
     return __funnelshift_r(lo, hi, s);
 }
 
+// Inclusive warp sum scan: five shfl.up steps whose in-range predicate
+// guards the add (no lane-index compares).
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v)
+{
+    asm volatile("{\n\t.reg .u32 t;\n\t.reg .pred p;\n\t"
+        "shfl.sync.up.b32 t|p, %0, 1, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
+        "shfl.sync.up.b32 t|p, %0, 2, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
+        "shfl.sync.up.b32 t|p, %0, 4, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
+        "shfl.sync.up.b32 t|p, %0, 8, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
+        "shfl.sync.up.b32 t|p, %0, 16, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t}"
+        : "+r"(v));
+    return v;
+}
+
 __device__ __forceinline__ uint32_t lane_id()
 {
     uint32_t l;

@@ -203,9 +203,9 @@ struct DirU8U16T {
     }
     template <bool B>
     __device__ static void compute(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, OutT *out_w,
-                                   const SelPair *sel, WarpResult &wr, uint32_t wit, const In &in)
+                                   const SelPair *sel, WarpResult &wr, uint32_t wit, const In &in, uint32_t &hint)
     {
-        u8u16_warp<B, BE>(base, tile_off, lo_b, hi_b, out_w, sel, wr, wit, in);
+        u8u16_warp<B, BE>(base, tile_off, lo_b, hi_b, out_w, sel, wr, wit, in, hint);
     }
     __device__ static void copy_out(const OutT *src, uint32_t cnt, OutT *out_a, uint64_t g0)
     {
@@ -227,7 +227,7 @@ struct DirU16U8T {
     }
     template <bool B>
     __device__ static void compute(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, OutT *out_w,
-                                   const SelPair *, WarpResult &wr, uint32_t wit, const In &in)
+                                   const SelPair *, WarpResult &wr, uint32_t wit, const In &in, uint32_t &)
     {
         u16u8_warp_r<B>(base, tile_off, lo_b, hi_b, out_w, wr, wit, in);
     }
@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     OutT *out_g = reinterpret_cast<OutT *>(smem_raw) + g * (2 * kGroupWarps * Dir::kStride);
 
     uint32_t i = 0;
+    uint32_t hint = 2; // K1: the warp's class-path prediction (u8_round_detect_spec)
     uint64_t st_pre = 0; // group thread 0: early poll of the next status word to resolve
     // group thread 0: the next tile; the ticket is taken right after the
     // tile-done barrier so its latency overlaps the combine + publish
@@ -360,9 +361,9 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
             break;
         OutT *out_w = out_g + (buf * kGroupWarps + wit) * Dir::kStride;
         if (interior)
-            Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in);
+            Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in, hint);
         else
-            Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in);
+            Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in, hint);
         LU_T(4); // compute
         // poll the status word resolved at the top of the next iteration now:
         // its L2 round trip overlaps the other warps' compute
@@ -412,60 +413,154 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
 
 // ================================================================= K3 / K4
 //
-// Warp-independent persistent validators: every warp walks 2 KiB chunks
-// (global warp id + i * total warps), with no CTA barrier and no staging.
-// A warp that finds an error publishes atomicMax(n - pos) and stops (its
-// later chunks all lie after the error); a warp also stops when a published
-// error lies before its next chunk (the reference stops at the first error
-// too).  The last warp to finish writes the result record.
-// ws layout: [u64 max(n - bad_pos)][u32 warps done][u32 pad].
+// Persistent validators fed by a TMA ring.  The input is cut into 16 KiB
+// stages (8 warp chunks of 2 KiB); CTA b takes stages b, b + grid, ...  Thread
+// 0 keeps kValStages stages in flight per CTA with cp.async.bulk (TMA bulk
+// copies, completion counted on an mbarrier per ring slot), each stage copied
+// with 16 bytes of look-behind and look-ahead so every warp finds its halo
+// quads in shared memory; warps read their chunk with LDS.128.  This keeps
+// ~200 KB of loads in flight per SM without prefetch registers (a register
+// double buffer cost occupancy; cp.async per warp measured slower).  The first
+// and last stages (whose +-16-byte window leaves [lo, hi)) are loaded
+// directly with masked loads.
+//
+// A warp that finds an error publishes atomicMax(n - pos); the CTA stops after
+// the stage in which one of its warps found an error, or once a published
+// error lies before its next stage (the reference stops at the first error).
+// The last warp to finish writes the result record.
+// ws layout: [u64 max(n - bad_pos)][u32 warps done][u32 pad][u64 count].
+
+constexpr int kValStages = 4;
+constexpr int kStageBytes = kWarps * kChunkBytes; // 16 KiB
+constexpr int kStageAlloc = kStageBytes + 32;      // + 16 B halo on each side
+constexpr size_t kSmemVal = (size_t)kValStages * kStageAlloc;
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
+{
+    asm volatile("{\n\t.reg .pred P;\n\tLU_W%=: mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t@!P bra LU_W%=;\n\t}" ::"r"(bar),
+                 "r"(parity)
+                 : "memory");
+}
 
 template <bool Utf16, bool Count = false, bool Swap16 = false>
-__global__ void __launch_bounds__(kThreads) k_validate_w(const uint8_t *__restrict__ base, uint32_t lead,
-                                                         uint64_t n, uint64_t *__restrict__ ws,
-                                                         Outcome *__restrict__ res, uint64_t nchunks)
+__global__ void __launch_bounds__(kThreads, 3) k_validate_w(const uint8_t *__restrict__ base, uint32_t lead,
+                                                            uint64_t n, uint64_t *__restrict__ ws,
+                                                            Outcome *__restrict__ res, uint64_t nstages)
 {
+    extern __shared__ __align__(128) uint8_t ring[];
+    __shared__ __align__(8) uint64_t bar[kValStages];
     __shared__ WarpResult wr_s[kWarps];
-    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t warp = tid >> 5;
     const uint32_t lane = lane_id();
     const uint64_t total_warps = (uint64_t)gridDim.x * kWarps;
     const uint64_t n_bytes = Utf16 ? 2 * n : n;
     const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n_bytes;
-    uint64_t best = 0;  // cached global max(n - bad_pos)
-    uint32_t count = 0; // Count: this lane's output units over the warp's chunks
-    // (a cp.async double buffer per warp measured 6-11% slower: the loads are
-    // already latency-hidden by 32 resident warps per SM)
-    for (uint64_t c = (uint64_t)blockIdx.x * kWarps + warp; c < nchunks; c += total_warps) {
-        const int64_t off = (int64_t)c * kChunkBytes;
-        if (best != 0 && lo_b + (Utf16 ? 2 : 1) * (int64_t)(n - best) < off)
-            break; // an earlier error is already known
-        const uint64_t best_next = *reinterpret_cast<volatile uint64_t *>(ws); // consumed next iteration
-        const bool interior = (off - 4 >= lo_b) && (off + kChunkBytes + 4 <= hi_b);
-        uint32_t err, pos, cc = 0;
-        if (Utf16) {
-            if (interior)
-                u16val_warp_r<false, Count, Swap16>(base, off, lo_b, hi_b, err, pos, &cc);
-            else
-                u16val_warp_r<true, Count, Swap16>(base, off, lo_b, hi_b, err, pos, &cc);
+    auto tma_ok = [&](uint64_t j) {
+        const int64_t s0 = (int64_t)j * kStageBytes;
+        return s0 - 16 >= lo_b && s0 + kStageBytes + 16 <= hi_b;
+    };
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bar[0]);
+    const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring);
+    auto issue = [&](uint64_t j, uint32_t slot) {
+        const uint32_t b = bar0 + 8 * slot;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kStageAlloc) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         ring0 + slot * kStageAlloc),
+                     "l"(base + (int64_t)j * kStageBytes - 16), "r"(kStageAlloc), "r"(b)
+                     : "memory");
+    };
+    if (tid == 0) {
+        for (int k = 0; k < kValStages; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * k));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (uint32_t k = 0; k < (uint32_t)kValStages; ++k) {
+            const uint64_t j = blockIdx.x + (uint64_t)k * gridDim.x;
+            if (j < nstages && tma_ok(j))
+                issue(j, k);
+        }
+    uint32_t hint = 2;    // K3: the warp's class-path prediction (u8_round_detect_spec)
+    uint32_t count = 0;   // Count: this lane's output units over the warp's chunks
+    uint32_t parity = 0;  // bit k: mbarrier phase of ring slot k
+    uint64_t i = 0, j = blockIdx.x;
+    for (; j < nstages; ++i, j += gridDim.x) {
+        const uint32_t slot = (uint32_t)(i % kValStages);
+        const int64_t off = (int64_t)j * kStageBytes + (int64_t)warp * kChunkBytes;
+        ChunkIn in;
+        const bool fast = tma_ok(j);
+        if (fast) {
+            mbar_wait(bar0 + 8 * slot, (parity >> slot) & 1);
+            parity ^= 1u << slot;
+            const uint8_t *sb = ring + slot * kStageAlloc + 16 + warp * kChunkBytes;
+#pragma unroll
+            for (int r = 0; r < kChunkBytes / 512; ++r) {
+                in.q[r] = *reinterpret_cast<const uint4 *>(sb + r * 512 + 16 * lane);
+                if (Swap16)
+                    in.q[r] = make_uint4(swap16x2(in.q[r].x), swap16x2(in.q[r].y), swap16x2(in.q[r].z),
+                                         swap16x2(in.q[r].w));
+            }
+            in.halo_p = *reinterpret_cast<const uint32_t *>(sb - 4);
+            in.halo_n = *reinterpret_cast<const uint32_t *>(sb + kChunkBytes);
+            if (Swap16) {
+                in.halo_p = swap16x2(in.halo_p);
+                in.halo_n = swap16x2(in.halo_n);
+            }
         } else {
-            if (interior)
-                u8val_warp<false, Count>(base, off, lo_b, hi_b, wr_s[warp], 0, &cc);
-            else
-                u8val_warp<true, Count>(base, off, lo_b, hi_b, wr_s[warp], 0, &cc);
-            __syncwarp();
-            err = wr_s[warp].err;
-            pos = wr_s[warp].pos;
+            load_chunk<true, Swap16>(base, off, lo_b, hi_b, in);
+        }
+        uint32_t err = 0, pos = 0, cc = 0;
+        if (off < hi_b) {
+            if (Utf16) {
+                if (fast)
+                    u16val_warp_in<false, Count>(off, lo_b, hi_b, in, err, pos, &cc);
+                else
+                    u16val_warp_in<true, Count>(off, lo_b, hi_b, in, err, pos, &cc);
+            } else {
+                if (fast)
+                    u8val_warp_in<false, Count>(base, off, lo_b, hi_b, in, wr_s[warp], 0, hint, &cc);
+                else
+                    u8val_warp_in<true, Count>(base, off, lo_b, hi_b, in, wr_s[warp], 0, hint, &cc);
+                __syncwarp();
+                err = wr_s[warp].err;
+                pos = wr_s[warp].pos;
+            }
         }
         count += cc;
-        if (err) {
-            if (lane == 0) {
-                const int64_t pb = off + pos - lo_b;
-                const uint64_t pu = Utf16 ? (uint64_t)(pb >> 1) : (uint64_t)pb;
-                atomicMax(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)(n - pu));
-            }
-            break;
+        if (err && lane == 0) {
+            const int64_t pb = off + pos - lo_b;
+            const uint64_t pu = Utf16 ? (uint64_t)(pb >> 1) : (uint64_t)pb;
+            atomicMax(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)(n - pu));
         }
-        best = best_next;
+        // stop after this stage if an error is known before the next one
+        bool stop_me = err != 0;
+        if (tid == 0) {
+            const uint64_t best = *reinterpret_cast<volatile uint64_t *>(ws);
+            const int64_t next0 = (int64_t)(j + gridDim.x) * kStageBytes;
+            stop_me |= best != 0 && lo_b + (Utf16 ? 2 : 1) * (int64_t)(n - best) < next0;
+        }
+        const bool stop = __syncthreads_or(stop_me); // also: every warp is done with the slot
+        if (stop)
+            break;
+        if (tid == 0) {
+            const uint64_t jn = j + (uint64_t)kValStages * gridDim.x;
+            if (jn < nstages && tma_ok(jn))
+                issue(jn, slot);
+        }
+    }
+    // an early stop leaves up to kValStages - 1 stages in flight: let them land
+    // before the CTA (and its shared memory) goes away
+    if (tid == 0 && j < nstages) {
+        for (uint32_t d = 1; d < (uint32_t)kValStages; ++d) {
+            const uint64_t jd = j + (uint64_t)d * gridDim.x;
+            const uint32_t slot = (uint32_t)((i + d) % kValStages);
+            if (jd < nstages && tma_ok(jd)) {
+                mbar_wait(bar0 + 8 * slot, (parity >> slot) & 1);
+                parity ^= 1u << slot;
+            }
+        }
     }
     if (Count) {
         const uint32_t wsum = __reduce_add_sync(0xffffffffu, count);
@@ -519,6 +614,7 @@ __global__ void __launch_bounds__(kThreads) k_batch(const uint8_t *__restrict__ 
         const int64_t lo_b = (int64_t)lead + ((int64_t)u0 << kShift);
         const int64_t hi_b = (int64_t)lead + ((int64_t)u1 << kShift);
         uint64_t running = 0, consumed = u1 - u0;
+        uint32_t hint = 2;
         uint32_t status = kStatusOk;
         for (int64_t chunk = lo_b & ~(int64_t)15; chunk < hi_b; chunk += kChunkBytes) {
             uint32_t err, pos, units = 0;
@@ -527,7 +623,7 @@ __global__ void __launch_bounds__(kThreads) k_batch(const uint8_t *__restrict__ 
                 load_chunk<true>(base, chunk, lo_b, hi_b, in);
                 if (Op == 0) {
                     uint16_t *stage = reinterpret_cast<uint16_t *>(smem_raw) + warp * kOutStrideU16;
-                    u8u16_warp<true>(base, chunk, lo_b, hi_b, stage, sel, wres[warp], 0, in);
+                    u8u16_warp<true>(base, chunk, lo_b, hi_b, stage, sel, wres[warp], 0, in, hint);
                     __syncwarp();
                     units = wres[warp].units;
                     copy_out_u16(stage, units, reinterpret_cast<uint16_t *>(out_a), out_lead + u0 + running);
@@ -541,7 +637,11 @@ __global__ void __launch_bounds__(kThreads) k_batch(const uint8_t *__restrict__ 
                 err = wres[warp].err;
                 pos = wres[warp].pos;
             } else if (Op == 2) {
-                u8val_warp<true>(base, chunk, lo_b, hi_b, wres[warp], 0);
+                {
+                    ChunkIn in;
+                    load_chunk<true>(base, chunk, lo_b, hi_b, in);
+                    u8val_warp_in<true>(base, chunk, lo_b, hi_b, in, wres[warp], 0, hint);
+                }
                 __syncwarp();
                 err = wres[warp].err;
                 pos = wres[warp].pos;
@@ -707,15 +807,20 @@ using namespace lu;
 
 template <bool Utf16, bool Count, bool Swap16 = false>
 static int launch_validate(const uint8_t *base, uint32_t lead, uint64_t n_units, void *ws, lu_outcome *res,
-                           uint64_t nchunks, cudaStream_t stream)
+                           uint64_t nbytes_frame, cudaStream_t stream)
 {
+    const void *fn = (const void *)k_validate_w<Utf16, Count, Swap16>;
+    const int sb = (int)kSmemVal;
+    if (int rc = ensure_smem_attr(8 + 4 * Utf16 + 2 * Count + Swap16, &fn, &sb, 1))
+        return rc;
+    const uint64_t nstages = (nbytes_frame + kStageBytes - 1) / kStageBytes;
     unsigned grid = 0;
-    int rc = persistent_grid((const void *)k_validate_w<Utf16, Count, Swap16>, kThreads, 0,
-                             (nchunks + kWarps - 1) / kWarps, &grid);
+    // at least one CTA: its last warp writes the result (also for empty input)
+    int rc = persistent_grid(fn, kThreads, kSmemVal, nstages ? nstages : 1, &grid);
     if (rc)
         return rc;
-    k_validate_w<Utf16, Count, Swap16><<<grid, kThreads, 0, stream>>>(
-        base, lead, n_units, reinterpret_cast<uint64_t *>(ws), reinterpret_cast<Outcome *>(res), nchunks);
+    k_validate_w<Utf16, Count, Swap16><<<grid, kThreads, kSmemVal, stream>>>(
+        base, lead, n_units, reinterpret_cast<uint64_t *>(ws), reinterpret_cast<Outcome *>(res), nstages);
     return 0;
 }
 
@@ -737,16 +842,16 @@ static int validate_impl(bool utf16, bool count, const uint8_t *inb, uint64_t n_
     if (e != cudaSuccess)
         return cuda_fail(e, "cudaMemsetAsync");
     const uint8_t *base = inb ? inb - lead : reinterpret_cast<const uint8_t *>(16);
-    const uint64_t nchunks = n_tiles(utf16 ? 2 * n_units : n_units, lead, kChunkBytes);
+    const uint64_t frame = lead + (utf16 ? 2 * n_units : n_units);
     int rc;
     if (utf16 && be)
-        rc = launch_validate<true, false, true>(base, lead, n_units, ws, res, nchunks, stream);
+        rc = launch_validate<true, false, true>(base, lead, n_units, ws, res, frame, stream);
     else if (utf16)
-        rc = count ? launch_validate<true, true>(base, lead, n_units, ws, res, nchunks, stream)
-                   : launch_validate<true, false>(base, lead, n_units, ws, res, nchunks, stream);
+        rc = count ? launch_validate<true, true>(base, lead, n_units, ws, res, frame, stream)
+                   : launch_validate<true, false>(base, lead, n_units, ws, res, frame, stream);
     else
-        rc = count ? launch_validate<false, true>(base, lead, n_units, ws, res, nchunks, stream)
-                   : launch_validate<false, false>(base, lead, n_units, ws, res, nchunks, stream);
+        rc = count ? launch_validate<false, true>(base, lead, n_units, ws, res, frame, stream)
+                   : launch_validate<false, false>(base, lead, n_units, ws, res, frame, stream);
     if (rc)
         return rc;
     e = cudaGetLastError();

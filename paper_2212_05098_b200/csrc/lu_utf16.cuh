@@ -176,13 +176,7 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
                     nb[k] = n0 + n1;
                     cnt += nb[k];
                 }
-                uint32_t incl = cnt;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-                    if (lane >= (uint32_t)d)
-                        incl += o;
-                }
+                const uint32_t incl = warp_incl_scan(cnt);
                 uint32_t off = running + incl - cnt;
                 // 1..5 bytes per quad (valid pairs: AA 2, AH 5, HL 4, LA 1, LH 4)
 #pragma unroll
@@ -243,13 +237,7 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
                 nb[k] = 2u + 2u * ((big >> 15 & 1u) + (big >> 31));
                 cnt += nb[k];
             }
-            uint32_t incl = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= (uint32_t)d)
-                    incl += o;
-            }
+            const uint32_t incl = warp_incl_scan(cnt);
             uint32_t off = running + incl - cnt;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -283,13 +271,7 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
                 nb[k] = 2u + (big >> 15 & 1u) + (big >> 31);
                 cnt += nb[k];
             }
-            uint32_t incl = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= (uint32_t)d)
-                    incl += o;
-            }
+            const uint32_t incl = warp_incl_scan(cnt);
             uint32_t off = running + incl - cnt;
             // 2..4 bytes per quad: two unconditional, two predicated stores
 #pragma unroll
@@ -345,13 +327,7 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
             cnt += l0 + l1;
             anybad |= bad[k];
         }
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= (uint32_t)d)
-                incl += o;
-        }
+        const uint32_t incl = warp_incl_scan(cnt);
         const uint32_t excl = incl - cnt;
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
         if (sur && __any_sync(0xffffffffu, anybad != 0)) {
@@ -407,70 +383,120 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
 }
 
 
+// High / low bytes of the four 16-bit words of two quads, one word per byte
+// (byte j of the result = word j of the pair a, b).
+__device__ __forceinline__ uint32_t hi_bytes(uint32_t a, uint32_t b) { return prmt(a, b, 0x7531u); }
+__device__ __forceinline__ uint32_t lo_bytes(uint32_t a, uint32_t b) { return prmt(a, b, 0x6420u); }
+
+// Surrogate masks of four words from their gathered high bytes: bit 7 of
+// byte j of ls is set iff word j is a low surrogate, and bit 7 of byte j of
+// nhs is CLEAR iff word j is a high surrogate (complemented: saves a NOT).
+// The other bits are garbage; callers only test bit 7 of each byte.  4 words
+// per 32-bit op instead of 2 (u16_sur_masks): high byte in D8..DF <=>
+// surrogate, bit 2 of it tells low from high.
+__device__ __forceinline__ void u16_sur4(uint32_t hb, uint32_t &nhs, uint32_t &ls)
+{
+    const uint32_t c = hb ^ 0xD8D8D8D8u;                 // zero top 5 bits <=> surrogate
+    const uint32_t u = (c & 0x78787878u) + 0x7F7F7F7Fu;  // bit 7: some of bits 3..6 set (no carry out)
+    const uint32_t b5 = hb << 5;                         // bit 2 -> bit 7
+    nhs = u | c | b5;
+    ls = ~(u | c) & b5;
+}
+
 // K4 warp body: validate one 2 KiB chunk (1024 words) in 4 rounds of 512 B,
 // lane l holding words [8l, 8l+8) in registers.  A low surrogate must sit
 // exactly where the previous word is a high surrogate, so the round is clean
-// iff ls == hs shifted by one word (one funnel shift per quad); a flagged
-// round is resolved with the exact predicate u16_bad2.
+// iff ls == hs shifted by one word.  The high bytes of a lane's 8 words are
+// gathered into two registers (one prmt each), so the masks and the shifted
+// compare cover 4 words per op; a flagged round is resolved with the exact
+// predicate u16_bad2.
 // Count = true also returns, in `count`, the UTF-8 length of the chunk's
 // words (1/2/3 bytes per BMP word, 4 per high surrogate, 0 per low one; exact
 // when the input is valid) -- utf8_length_from_utf16le.
-template <bool Boundary, bool Count = false, bool Swap16 = false>
-__device__ __forceinline__ void u16val_warp_r(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
-                                              int64_t hi_b, uint32_t &err, uint32_t &err_pos,
-                                              uint32_t *count = nullptr)
+// `in` holds the chunk (load_chunk<Boundary, Swap16>), loaded by the caller so
+// it can be prefetched a chunk ahead.
+template <bool Boundary, bool Count = false>
+__device__ __forceinline__ void u16val_warp_in(int64_t tile_off, int64_t lo_b, int64_t hi_b, const ChunkIn &in,
+                                               uint32_t &err, uint32_t &err_pos, uint32_t *count = nullptr)
 {
     const uint32_t lane = lane_id();
     const int64_t chunk = tile_off;
     constexpr int kRounds = kChunkBytes / 512;
-    ChunkIn in;
-    load_chunk<Boundary, Swap16>(base, chunk, lo_b, hi_b, in);
     const uint4 *q = in.q;
-    uint32_t carry = in.halo_p;
-    const uint32_t halo_n = in.halo_n;
+    // hs of the word before the round, at byte 3 (lane 0: carried across rounds)
+    uint32_t hcarry;
+    {
+        uint32_t hsh, lsh;
+        u16_sur4(hi_bytes(in.halo_p, in.halo_p), hsh, lsh);
+        hcarry = hsh;
+    }
     uint32_t cnt = 0;
-    uint32_t rn[kRounds];
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r)
-        rn[r] = __shfl_sync(0xffffffffu, q[r].x, (lane + 1) & 31);
     err = 0;
     err_pos = 0;
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
-        const uint32_t rp = __shfl_sync(0xffffffffu, q[r].w, (lane + 31) & 31);
-        uint32_t w[6];
-        w[0] = (lane == 0) ? carry : rp;
-        carry = rp;
-        w[1] = q[r].x;
-        w[2] = q[r].y;
-        w[3] = q[r].z;
-        w[4] = q[r].w;
-        w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : halo_n) : rn[r];
-        uint32_t hs[6], ls[6];
-#pragma unroll
-        for (int k = 0; k < 6; ++k)
-            u16_sur_masks(w[k], hs[k], ls[k]);
-        uint32_t det = 0;
-#pragma unroll
-        for (int k = 1; k <= 5; ++k)
-            det |= ls[k] ^ fsl(hs[k - 1], hs[k], 16);
+        const uint32_t hbA = hi_bytes(q[r].x, q[r].y), hbB = hi_bytes(q[r].z, q[r].w);
+        uint32_t hsA, lsA, hsB, lsB;
+        u16_sur4(hbA, hsA, lsA);
+        u16_sur4(hbB, hsB, lsB);
+        const uint32_t rp = __shfl_sync(0xffffffffu, hsB, (lane + 31) & 31);
+        const uint32_t hsp = (lane == 0) ? hcarry : rp;
+        hcarry = rp;
+        // (hs complemented) bit 7 of ok is set where ls == hs of the previous word
+        uint32_t ok = (lsA ^ fsl(hsp, hsA, 8)) & (lsB ^ fsl(hsA, hsB, 8));
+        if (r == kRounds - 1 && lane == 31) {
+            // chunk end: the word after the chunk must match the last hs
+            uint32_t hsN, lsN;
+            u16_sur4(in.halo_n >> 8, hsN, lsN);
+            ok &= (lsN ^ (hsB >> 24)) | 0xFFFFFF00u;
+        }
+        const uint32_t det = ~ok & H8;
         if (Count) {
+            const uint32_t lbA = lo_bytes(q[r].x, q[r].y), lbB = lo_bytes(q[r].z, q[r].w);
 #pragma unroll
-            for (int k = 1; k <= 4; ++k) {
-                const uint32_t x = w[k];
-                const uint32_t a = x & 0xFF80FF80u, b = x & 0xF800F800u;
-                const uint32_t big = (((a & 0x7FFF7FFFu) + 0x7FFF7FFFu) | a) & 0x80008000u; // word >= 0x80
-                const uint32_t mid = (((b & 0x7FFF7FFFu) + 0x7FFF7FFFu) | b) & 0x80008000u; // word >= 0x800
-                uint32_t one = 0x80008000u;
+            for (int g = 0; g < 2; ++g) {
+                const uint32_t hb = g ? hbB : hbA, lb = g ? lbB : lbA;
+                const uint32_t z = hb | (lb & H8);
+                const uint32_t big = (((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) & H8;  // word >= 0x80
+                const uint32_t mid = (((hb & 0x78787878u) + 0x7F7F7F7Fu) | hb) & H8; // word >= 0x800
+                uint32_t one = H8;
                 if (Boundary) {
-                    const uint32_t v = valid_words(chunk + r * 512 + 16 * (int64_t)lane + 4 * (k - 1), lo_b, hi_b);
-                    one = ((v & 1) ? 0x8000u : 0u) | ((v & 2) ? 0x80000000u : 0u);
+                    const int64_t a = chunk + r * 512 + 16 * (int64_t)lane + 8 * g;
+                    const uint32_t v = valid_words(a, lo_b, hi_b) | (valid_words(a + 4, lo_b, hi_b) << 2);
+                    one = ((v & 1) ? 0x80u : 0u) | ((v & 2) ? 0x8000u : 0u) | ((v & 4) ? 0x800000u : 0u) |
+                          ((v & 8) ? 0x80000000u : 0u);
                 }
+                const uint32_t hs = ~(g ? hsB : hsA) & H8, ls = (g ? lsB : lsA) & H8;
                 // out-of-range words read as 0: no big/mid/surrogate bits
-                cnt += __popc(one) + __popc(big) + __popc(mid) + __popc(hs[k]) - 3 * __popc(ls[k]);
+                cnt += __popc(one) + __popc(big) + __popc(mid) + __popc(hs) - 3 * __popc(ls);
             }
         }
         if (__any_sync(0xffffffffu, det != 0)) {
+            // rare: exact predicate on the raw words (neighbour quads by shuffle)
+            const uint32_t prevw = __shfl_sync(0xffffffffu, r > 0 ? q[r > 0 ? r - 1 : 0].w : 0u, 31);
+            const uint32_t nextw = __shfl_sync(0xffffffffu, r + 1 < kRounds ? q[r + 1 < kRounds ? r + 1 : r].x : 0u, 0);
+            const uint32_t rpw = __shfl_sync(0xffffffffu, q[r].w, (lane + 31) & 31);
+            const uint32_t rnw = __shfl_sync(0xffffffffu, q[r].x, (lane + 1) & 31);
+            uint32_t w[6];
+            w[0] = (lane == 0) ? (r == 0 ? in.halo_p : prevw) : rpw;
+            w[1] = q[r].x;
+            w[2] = q[r].y;
+            w[3] = q[r].z;
+            w[4] = q[r].w;
+            w[5] = (lane == 31) ? (r + 1 < kRounds ? nextw : in.halo_n) : rnw;
+            if (r > 0) {
+                // the pair (last word of the previous round, first word of
+                // this one) is only compared here: a high surrogate ending
+                // the previous round without its low surrogate comes first
+                uint32_t tb = (lane == 0 && is_hs(w[0] >> 16) && !is_ls(w[1] & 0xFFFFu)) ? 1u : 0u;
+                if (Boundary && tb)
+                    tb = valid_words(chunk + r * 512 - 4, lo_b, hi_b) >> 1;
+                if (__shfl_sync(0xffffffffu, tb, 0)) {
+                    err = 1;
+                    err_pos = (uint32_t)(r * 512) - 2;
+                    return;
+                }
+            }
             const int64_t lane_off = chunk + r * 512 + 16 * (int64_t)lane;
             uint32_t kb = 8;
 #pragma unroll
@@ -492,6 +518,16 @@ __device__ __forceinline__ void u16val_warp_r(const uint8_t *__restrict__ base, 
     }
     if (Count)
         *count = cnt;
+}
+
+template <bool Boundary, bool Count = false, bool Swap16 = false>
+__device__ __forceinline__ void u16val_warp_r(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
+                                              int64_t hi_b, uint32_t &err, uint32_t &err_pos,
+                                              uint32_t *count = nullptr)
+{
+    ChunkIn in;
+    load_chunk<Boundary, Swap16>(base, tile_off, lo_b, hi_b, in);
+    u16val_warp_in<Boundary, Count>(tile_off, lo_b, hi_b, in, err, err_pos, count);
 }
 
 } // namespace lu

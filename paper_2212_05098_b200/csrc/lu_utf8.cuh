@@ -237,6 +237,147 @@ __device__ __forceinline__ void u8_round_detect(U8Round &R)
     R.det = det;
 }
 
+// chunk end (lane 31, last round): leads of the last quad whose
+// continuations would lie past the chunk, checked against the halo quad
+__device__ __forceinline__ uint32_t u8_chunk_end_check(const U8Round &R)
+{
+    const uint32_t cn = u8_classify(R.w[5]).C;
+    const U8Masks &m = R.m[4];
+    return (m.L & ~fsr(m.C, cn, 8)) | (m.E & ~fsr(m.C, cn, 16)) | (m.F & ~fsr(m.C, cn, 24));
+}
+
+// Speculative per-class detectors.  A warp predicts that a round has the same
+// class mix as its previous one (the path `hint`) and runs only that path's
+// detector, which flags every bad byte the path's class can contain AND every
+// byte outside the class (a lead of another length, a continuation the class
+// cannot claim).  If nothing is flagged anywhere in the warp the prediction
+// holds and the round takes that path with det = 0, so one vote replaces the
+// general detector's two to four class votes; otherwise the general detector
+// (u8_round_detect) runs and its path becomes the next hint.  The masks are
+// filled as the path's decoder and chunk-end check expect (exact when the
+// prediction holds).
+//
+// "Must be a continuation" is computed arithmetically on the FMA pipe where
+// the class allows it: for path 1 it is E(i-1) | E(i-2) = E * 0x10100 (low
+// word) plus the previous quad's spill (high word of the same product); for
+// path 3, F * 0x01010100.  Terms overlap only where a lead follows a lead
+// that needed a continuation, which is flagged one byte earlier, so the sum
+// (carries fall outside bit 7 or onto already-flagged bytes) is as good as
+// the OR.  Returns a value whose bit 7 bytes flag; other bits are garbage.
+
+// path 0: ASCII and 2-byte leads only
+__device__ __forceinline__ uint32_t u8_fast0(U8Round &R)
+{
+    uint32_t Lp;
+    {
+        const uint32_t x = R.w[0];
+        Lp = x & (x << 1) & H8;
+    }
+    uint32_t det = 0;
+#pragma unroll
+    for (int k = 1; k <= 4; ++k) {
+        const uint32_t x = R.w[k];
+        const uint32_t t1 = x << 1;
+        const uint32_t C = x & ~t1 & H8, L = x & t1 & H8;
+        det |= fsl(Lp, L, 8) ^ C;                          // continuation structure
+        det |= L & (x << 2);                               // a lead >= E0: not this class
+        det |= L & ~((x & 0x1E1E1E1Eu) + 0x7F7F7F7Fu);      // C0 / C1
+        R.m[k].C = C;
+        R.m[k].L = L;
+        R.m[k].E = 0;
+        R.m[k].F = 0;
+        Lp = L;
+    }
+    return det & H8;
+}
+
+// path 1: ASCII and 3-byte leads only
+__device__ __forceinline__ uint32_t u8_fast1(U8Round &R)
+{
+    uint32_t Ep;
+    {
+        const uint32_t x = R.w[0];
+        Ep = x & (x << 1) & (x << 2) & H8;
+    }
+    uint32_t spill = __umulhi(Ep, 0x10100u);
+    uint32_t det = 0;
+#pragma unroll
+    for (int k = 1; k <= 4; ++k) {
+        const uint32_t x = R.w[k];
+        const uint32_t t1 = x << 1, t2 = x << 2;
+        const uint32_t C = x & ~t1 & H8, L = x & t1 & H8;
+        const uint32_t E = L & t2;
+        const uint32_t need = E * 0x10100u + spill;        // E(i-1) | E(i-2)
+        spill = __umulhi(E, 0x10100u);
+        det |= need ^ C;
+        det |= L & ~t2;                                    // a 2-byte lead: not this class
+        det |= E & (x << 3);                               // an F-class byte: not this class
+        const uint32_t v = x + 0x03030303u;                // E0 / ED candidates (u8_prefilter_e)
+        det |= E & ~(v << 4) & ~(v << 5);
+        R.m[k].C = C;
+        R.m[k].L = E;
+        R.m[k].E = E;
+        R.m[k].F = 0;
+    }
+    return det & H8;
+}
+
+// path 3: ASCII and 4-byte leads only (text outside the BMP, e.g. emoji)
+__device__ __forceinline__ uint32_t u8_fast3(U8Round &R)
+{
+    {
+        const uint32_t x = R.w[0];
+        R.m[0].F = x & (x << 1) & (x << 2) & (x << 3) & H8;
+    }
+    uint32_t spill = __umulhi(R.m[0].F, 0x01010100u);
+    uint32_t det = 0;
+#pragma unroll
+    for (int k = 1; k <= 4; ++k) {
+        const uint32_t x = R.w[k];
+        const uint32_t t1 = x << 1;
+        const uint32_t C = x & ~t1 & H8, L = x & t1 & H8;
+        const uint32_t F = L & (x << 2) & (x << 3);
+        const uint32_t need = F * 0x01010100u + spill;     // F(i-1) | F(i-2) | F(i-3)
+        spill = __umulhi(F, 0x01010100u);
+        det |= need ^ C;
+        det |= L & ~F;                                     // a 2- or 3-byte lead: not this class
+        det |= u8_check_f(x, fsr(x, R.w[k + 1], 8), U8Masks{C, L, F, F});
+        R.m[k].C = C;
+        R.m[k].L = F;
+        R.m[k].E = F;
+        R.m[k].F = F;
+    }
+    return det & H8;
+}
+
+// Round detection with the warp's path prediction (see above); hint is
+// warp-uniform, updated to the round's actual path on a miss.
+__device__ __forceinline__ void u8_round_detect_spec(U8Round &R, uint32_t &hint)
+{
+    uint32_t fd;
+    switch (hint) {
+    case 0:
+        fd = u8_fast0(R);
+        break;
+    case 1:
+        fd = u8_fast1(R);
+        break;
+    case 3:
+        fd = u8_fast3(R);
+        break;
+    default:
+        fd = 1;
+        break;
+    }
+    if (__any_sync(0xffffffffu, fd != 0)) {
+        u8_round_detect(R);
+        hint = (uint32_t)R.path;
+    } else {
+        R.path = (int)hint;
+        R.det = 0;
+    }
+}
+
 // ============================================================ K1: utf8->utf16
 
 struct alignas(8) SelPair {
@@ -326,12 +467,165 @@ __device__ __forceinline__ void sts16_if(uint32_t addr, uint32_t v, uint32_t roo
                  : "memory");
 }
 
+// One round's emit masks, scan, exact error resolution, decode and
+// compaction for a statically known class path P (0, 1, 3; 2 = general), so
+// each path's live ranges stay separate.
+template <int P, bool Boundary, bool BE>
+__device__ __forceinline__ void u8u16_round(const U8Round &R, int r, const uint8_t *__restrict__ base, int64_t tile_off,
+                                            int64_t chunk, int64_t lane_off, int64_t lo_b, int64_t hi_b,
+                                            uint32_t sbase, const SelPair *sel, uint32_t &running, uint32_t &err,
+                                            uint32_t &err_pos, uint32_t &units)
+{
+    const uint32_t lane = lane_id();
+    uint32_t e[4], fi1[4], c[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (P >= 2) {
+            fi1[k] = fsl(R.m[k].F, R.m[k + 1].F, 8);
+            e[k] = (~R.m[k + 1].C | fi1[k]) & H8;
+        } else {
+            fi1[k] = 0;
+            e[k] = ~R.m[k + 1].C & H8;
+        }
+        if (Boundary)
+            e[k] &= valid_mask(lane_off + 4 * k, lo_b, hi_b);
+        c[k] = (uint32_t)__popc(e[k]);
+    }
+    const uint32_t cnt = c[0] + c[1] + c[2] + c[3];
+    const uint32_t incl = warp_incl_scan(cnt);
+    const uint32_t excl = incl - cnt;
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+
+    if (__any_sync(0xffffffffu, R.det != 0)) {
+        // exact resolution in stream order: tail of the previous round first
+        const int64_t rstart = chunk + r * 512;
+        bool found = false;
+        if (r > 0) {
+            uint32_t tb = 3;
+            if (lane == 0) {
+                for (uint32_t t = 0; t < 3; ++t)
+                    if (u8_bad_global(base, rstart - 3 + t, lo_b, hi_b)) {
+                        tb = t;
+                        break;
+                    }
+            }
+            tb = __shfl_sync(0xffffffffu, tb, 0);
+            if (tb < 3) {
+                uint32_t drop = 0;
+                if (lane == 0) {
+                    // emits of the previous round's last quad at or after the error
+                    const uint32_t eq = u8_emit_global(base, rstart - 4, lo_b, hi_b);
+                    drop = (uint32_t)__popc(eq & ~((1u << (8 * (1 + tb))) - 1u));
+                }
+                drop = __shfl_sync(0xffffffffu, drop, 0);
+                err = 1;
+                err_pos = (uint32_t)(rstart - 3 + tb - tile_off);
+                units = running - drop;
+                found = true;
+            }
+        }
+        if (!found) {
+            // a lead missing a continuation is flagged at the continuation
+            // slot, possibly in the next lane: scan when either lane flagged
+            const uint32_t scan = R.det | __shfl_down_sync(0xffffffffu, R.det, 1);
+            uint32_t kb = 16;
+            if (scan != 0) {
+                for (uint32_t t = 0; t < 16; ++t)
+                    if (u8_bad_global(base, lane_off + t, lo_b, hi_b)) {
+                        kb = t;
+                        break;
+                    }
+            }
+            const uint32_t bm = __ballot_sync(0xffffffffu, kb < 16);
+            if (bm) {
+                const uint32_t fl = (uint32_t)__ffs(bm) - 1;
+                uint32_t em = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    em |= ((e[k] * 0x00204081u) >> 28) << (4 * k);
+                const uint32_t within = excl + (uint32_t)__popc(em & ((1u << (kb & 15)) - 1u));
+                const uint32_t kbf = __shfl_sync(0xffffffffu, kb, fl);
+                const uint32_t wf = __shfl_sync(0xffffffffu, within, fl);
+                err = 1;
+                err_pos = (uint32_t)(rstart - tile_off) + 16 * fl + kbf;
+                units = running + wf;
+            }
+        }
+    }
+
+    // decode + compact into the warp's staging region
+    bool any4 = false;
+    if (P == 2) {
+        uint32_t f4 = R.m[0].F;
+#pragma unroll
+        for (int k = 1; k <= 4; ++k)
+            f4 |= R.m[k].F;
+        any4 = __any_sync(0xffffffffu, f4 != 0);
+    }
+    uint32_t lop[4], hip[4];
+    if (P == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            u8_decode2(R.w[k + 1], R.w[k + 2], lop[k], hip[k]);
+    } else if (P == 1) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            u8_decode3(R.w[k + 1], R.w[k + 2], lop[k], hip[k]);
+    } else if (P == 3) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            u8_decode4(R.w[k + 1], R.w[k + 2], R.m[k + 1], lop[k], hip[k]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            u8_decode_quad(R.w[k + 1], R.w[k + 2], R.m[k + 1], fi1[k], any4, lop[k], hip[k]);
+    }
+    uint32_t off = running + excl;
+    const uint32_t lane_end = off + cnt;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t lo = lop[k], hi = hip[k];
+        const uint32_t idx = (e[k] * 0x00204081u) >> 28;
+        const SelPair sp = sel[idx];
+        const uint32_t w01 = BE ? prmt(hi, lo, sp.s01) : prmt(lo, hi, sp.s01);
+        const uint32_t w23 = BE ? prmt(hi, lo, sp.s23) : prmt(lo, hi, sp.s23);
+        const uint32_t a = sbase + 2 * off;
+        const uint32_t room = lane_end - off;
+        // Stores past this quad's words are overwritten by the next
+        // quad's stores (program order); only slots that valid input
+        // could push into the next lane's region are predicated.
+        if (Boundary) {
+            sts16_if(a, w01, room, 0);
+            sts16_if(a + 2, w01 >> 16, room, 1);
+            sts16_if(a + 4, w23, room, 2);
+            sts16_if(a + 6, w23 >> 16, room, 3);
+        } else {
+            sts16(a, w01);
+            if (k < 3)
+                sts16(a + 2, w01 >> 16);
+            else
+                sts16_if(a + 2, w01 >> 16, room, 1);
+            if (k < 2)
+                sts16(a + 4, w23);
+            else
+                sts16_if(a + 4, w23, room, 2);
+            if (k < 1)
+                sts16(a + 6, w23 >> 16);
+            else
+                sts16_if(a + 6, w23 >> 16, room, 3);
+        }
+        off += c[k];
+    }
+    running += tot;
+}
+
 // BE: emit UTF-16BE (the word's high byte first): the compaction prmt takes
 // its two byte planes in the other order, at no cost.
 template <bool Boundary, bool BE = false>
 __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
                                            int64_t hi_b, uint16_t *out_w, const SelPair *sel, WarpResult &wr,
-                                           uint32_t warp /* warp index inside the tile */, const ChunkIn &in)
+                                           uint32_t warp /* warp index inside the tile */, const ChunkIn &in,
+                                           uint32_t &hint)
 {
     const uint32_t lane = lane_id();
     const int64_t chunk = tile_off + (int64_t)warp * kChunkBytes;
@@ -359,159 +653,31 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
         R.w[3] = q[r].z;
         R.w[4] = q[r].w;
         R.w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : halo_n) : rn[r];
-        u8_round_detect(R);
-        if (r == kRounds - 1 && lane == 31) {
-            // chunk end: leads of the last quad whose continuations lie past the chunk
-            const uint32_t cn = u8_classify(R.w[5]).C;
-            const U8Masks &m = R.m[4];
-            R.det |= (m.L & ~fsr(m.C, cn, 8)) | (m.E & ~fsr(m.C, cn, 16)) | (m.F & ~fsr(m.C, cn, 24));
+        // predicted class path first (u8_round_detect_spec); the general
+        // detector and decoder only when the prediction misses
+        bool fast = false;
+#define LU_FAST_ROUND(PP, FN)                                                                                          \
+    if (hint == PP) {                                                                                                  \
+        const uint32_t fd = FN(R);                                                                                     \
+        if (!__any_sync(0xffffffffu, fd != 0)) {                                                                       \
+            fast = true;                                                                                               \
+            R.path = PP;                                                                                               \
+            R.det = (r == kRounds - 1 && lane == 31) ? u8_chunk_end_check(R) : 0u;                                     \
+            u8u16_round<PP, Boundary, BE>(R, r, base, tile_off, chunk, lane_off, lo_b, hi_b, sbase, sel, running, err, \
+                                          err_pos, units);                                                             \
+        }                                                                                                              \
+    }
+        LU_FAST_ROUND(0, u8_fast0)
+        else LU_FAST_ROUND(1, u8_fast1) else LU_FAST_ROUND(3, u8_fast3)
+#undef LU_FAST_ROUND
+        if (!fast) {
+            u8_round_detect(R);
+            hint = (uint32_t)R.path;
+            if (r == kRounds - 1 && lane == 31)
+                R.det |= u8_chunk_end_check(R);
+            u8u16_round<2, Boundary, BE>(R, r, base, tile_off, chunk, lane_off, lo_b, hi_b, sbase, sel, running, err,
+                                         err_pos, units);
         }
-        uint32_t e[4], fi1[4], c[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (R.path >= 2) {
-                fi1[k] = fsl(R.m[k].F, R.m[k + 1].F, 8);
-                e[k] = (~R.m[k + 1].C | fi1[k]) & H8;
-            } else {
-                fi1[k] = 0;
-                e[k] = ~R.m[k + 1].C & H8;
-            }
-            if (Boundary)
-                e[k] &= valid_mask(lane_off + 4 * k, lo_b, hi_b);
-            c[k] = (uint32_t)__popc(e[k]);
-        }
-        const uint32_t cnt = c[0] + c[1] + c[2] + c[3];
-        uint32_t incl = cnt;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= (uint32_t)d)
-                incl += o;
-        }
-        const uint32_t excl = incl - cnt;
-        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-
-        if (__any_sync(0xffffffffu, R.det != 0)) {
-            // exact resolution in stream order: tail of the previous round first
-            const int64_t rstart = chunk + r * 512;
-            bool found = false;
-            if (r > 0) {
-                uint32_t tb = 3;
-                if (lane == 0) {
-                    for (uint32_t t = 0; t < 3; ++t)
-                        if (u8_bad_global(base, rstart - 3 + t, lo_b, hi_b)) {
-                            tb = t;
-                            break;
-                        }
-                }
-                tb = __shfl_sync(0xffffffffu, tb, 0);
-                if (tb < 3) {
-                    uint32_t drop = 0;
-                    if (lane == 0) {
-                        // emits of the previous round's last quad at or after the error
-                        const uint32_t eq = u8_emit_global(base, rstart - 4, lo_b, hi_b);
-                        drop = (uint32_t)__popc(eq & ~((1u << (8 * (1 + tb))) - 1u));
-                    }
-                    drop = __shfl_sync(0xffffffffu, drop, 0);
-                    err = 1;
-                    err_pos = (uint32_t)(rstart - 3 + tb - tile_off);
-                    units = running - drop;
-                    found = true;
-                }
-            }
-            if (!found) {
-                // a lead missing a continuation is flagged at the continuation
-                // slot, possibly in the next lane: scan when either lane flagged
-                const uint32_t scan = R.det | __shfl_down_sync(0xffffffffu, R.det, 1);
-                uint32_t kb = 16;
-                if (scan != 0) {
-                    for (uint32_t t = 0; t < 16; ++t)
-                        if (u8_bad_global(base, lane_off + t, lo_b, hi_b)) {
-                            kb = t;
-                            break;
-                        }
-                }
-                const uint32_t bm = __ballot_sync(0xffffffffu, kb < 16);
-                if (bm) {
-                    const uint32_t fl = (uint32_t)__ffs(bm) - 1;
-                    uint32_t em = 0;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        em |= ((e[k] * 0x00204081u) >> 28) << (4 * k);
-                    const uint32_t within = excl + (uint32_t)__popc(em & ((1u << (kb & 15)) - 1u));
-                    const uint32_t kbf = __shfl_sync(0xffffffffu, kb, fl);
-                    const uint32_t wf = __shfl_sync(0xffffffffu, within, fl);
-                    err = 1;
-                    err_pos = (uint32_t)(rstart - tile_off) + 16 * fl + kbf;
-                    units = running + wf;
-                }
-            }
-        }
-
-        // decode + compact into the warp's staging region
-        bool any4 = false;
-        if (R.path == 2) {
-            uint32_t f4 = R.m[0].F;
-#pragma unroll
-            for (int k = 1; k <= 4; ++k)
-                f4 |= R.m[k].F;
-            any4 = __any_sync(0xffffffffu, f4 != 0);
-        }
-        uint32_t lop[4], hip[4];
-        if (R.path == 0) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                u8_decode2(R.w[k + 1], R.w[k + 2], lop[k], hip[k]);
-        } else if (R.path == 1) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                u8_decode3(R.w[k + 1], R.w[k + 2], lop[k], hip[k]);
-        } else if (R.path == 3) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                u8_decode4(R.w[k + 1], R.w[k + 2], R.m[k + 1], lop[k], hip[k]);
-        } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                u8_decode_quad(R.w[k + 1], R.w[k + 2], R.m[k + 1], fi1[k], any4, lop[k], hip[k]);
-        }
-        uint32_t off = running + excl;
-        const uint32_t lane_end = off + cnt;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t lo = lop[k], hi = hip[k];
-            const uint32_t idx = (e[k] * 0x00204081u) >> 28;
-            const SelPair sp = sel[idx];
-            const uint32_t w01 = BE ? prmt(hi, lo, sp.s01) : prmt(lo, hi, sp.s01);
-            const uint32_t w23 = BE ? prmt(hi, lo, sp.s23) : prmt(lo, hi, sp.s23);
-            const uint32_t a = sbase + 2 * off;
-            const uint32_t room = lane_end - off;
-            // Stores past this quad's words are overwritten by the next
-            // quad's stores (program order); only slots that valid input
-            // could push into the next lane's region are predicated.
-            if (Boundary) {
-                sts16_if(a, w01, room, 0);
-                sts16_if(a + 2, w01 >> 16, room, 1);
-                sts16_if(a + 4, w23, room, 2);
-                sts16_if(a + 6, w23 >> 16, room, 3);
-            } else {
-                sts16(a, w01);
-                if (k < 3)
-                    sts16(a + 2, w01 >> 16);
-                else
-                    sts16_if(a + 2, w01 >> 16, room, 1);
-                if (k < 2)
-                    sts16(a + 4, w23);
-                else
-                    sts16_if(a + 4, w23, room, 2);
-                if (k < 1)
-                    sts16(a + 6, w23 >> 16);
-                else
-                    sts16_if(a + 6, w23 >> 16, room, 3);
-            }
-            off += c[k];
-        }
-        running += tot;
         if (err)
             break;
     }
@@ -529,21 +695,21 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
 // Count = true also returns, in `count`, the UTF-16 length of the chunk
 // (one word per non-continuation byte plus one per 4-byte lead; exact when the
 // input is valid) -- utf16_length_from_utf8.
+// `in` holds the chunk at tile_off + warp * kChunkBytes (load_chunk<Boundary>),
+// loaded by the caller so it can be prefetched a chunk ahead.
 template <bool Boundary, bool Count = false>
-__device__ __forceinline__ void u8val_warp(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
-                                           int64_t hi_b, WarpResult &wr, uint32_t warp /* warp index in tile */,
-                                           uint32_t *count = nullptr)
+__device__ __forceinline__ void u8val_warp_in(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
+                                              int64_t hi_b, const ChunkIn &in, WarpResult &wr,
+                                              uint32_t warp /* warp index in tile */, uint32_t &hint,
+                                              uint32_t *count = nullptr)
 {
     uint32_t cnt = 0;
     const uint32_t lane = lane_id();
     const int64_t chunk = tile_off + (int64_t)warp * kChunkBytes;
     constexpr int kRounds = kChunkBytes / 512;
-    uint4 q[kRounds];
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r)
-        q[r] = ld16(base, chunk + r * 512 + 16 * (int64_t)lane, lo_b, hi_b, Boundary);
-    uint32_t carry = (lane == 0) ? halo4<Boundary>(base, chunk - 4, lo_b, hi_b) : 0u;
-    const uint32_t halo_n = (lane == 31) ? halo4<Boundary>(base, chunk + kChunkBytes, lo_b, hi_b) : 0u;
+    const uint4 *q = in.q;
+    uint32_t carry = in.halo_p;
+    const uint32_t halo_n = in.halo_n;
     uint32_t rn[kRounds];
 #pragma unroll
     for (int r = 0; r < kRounds; ++r)
@@ -560,7 +726,7 @@ __device__ __forceinline__ void u8val_warp(const uint8_t *__restrict__ base, int
         R.w[3] = q[r].z;
         R.w[4] = q[r].w;
         R.w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : halo_n) : rn[r];
-        u8_round_detect(R);
+        u8_round_detect_spec(R, hint);
         if (r == kRounds - 1 && lane == 31) {
             const uint32_t cn = u8_classify(R.w[5]).C;
             const U8Masks &m = R.m[4];
@@ -617,6 +783,17 @@ __device__ __forceinline__ void u8val_warp(const uint8_t *__restrict__ base, int
     }
     if (Count)
         *count = cnt;
+}
+
+template <bool Boundary, bool Count = false>
+__device__ __forceinline__ void u8val_warp(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
+                                           int64_t hi_b, WarpResult &wr, uint32_t warp /* warp index in tile */,
+                                           uint32_t *count = nullptr)
+{
+    ChunkIn in;
+    load_chunk<Boundary>(base, tile_off + (int64_t)warp * kChunkBytes, lo_b, hi_b, in);
+    uint32_t hint = 2;
+    u8val_warp_in<Boundary, Count>(base, tile_off, lo_b, hi_b, in, wr, warp, hint, count);
 }
 
 } // namespace lu
