@@ -487,3 +487,41 @@ def test_config5_full_size_single_gpu(cuda_ok, utf16):
             del rr, oo, got
         status, consumed, written, offsets = shard.combine_records(records, cuts[:-1])
         assert (status, consumed, written) == (0, units, whole.written)
+
+
+# ------------------------------------------------ class-path prediction
+
+
+def _class_switching_buffer(seed: int, utf16: bool, total: int = 3 << 20) -> bytes:
+    """Valid text whose class mix changes every few hundred bytes, so the
+    kernels' per-warp class-path prediction (u8_round_detect_spec) misses and
+    recovers at round, chunk and tile boundaries all the time."""
+    rng = random.Random(seed)
+    parts, n = [], 0
+    names = ["latin", "cyrillic", "cjk", "emoji", "mix"]
+    while n < total:
+        size = rng.choice([rng.randint(4, 64), rng.randint(100, 700), rng.randint(1500, 5000)])
+        if utf16:
+            size = max(2, size // 2)
+        t = corpus.generate(rng.choice(names), size, rng.randint(0, 1 << 30), utf16=utf16)
+        b = t.numpy().tobytes()
+        parts.append(b)
+        n += len(b)
+    return b"".join(parts)
+
+
+@pytest.mark.parametrize("utf16", [False, True])
+def test_class_switching_text(cuda_ok, utf16):
+    data = _class_switching_buffer(11 + utf16, utf16)
+    check = check_u16 if utf16 else check_u8
+    check(data)
+    rng = random.Random(5 + utf16)
+    unit = 2 if utf16 else 1
+    for _ in range(12):
+        b = bytearray(data)
+        pos = rng.randrange(0, len(b) // unit) * unit
+        if utf16:
+            b[pos:pos + 2] = rng.choice([0xD800, 0xDC00, 0xDBFF, 0xDFFF]).to_bytes(2, "little")
+        else:
+            b[pos] = rng.choice([0x80, 0xBF, 0xC0, 0xC1, 0xE0, 0xED, 0xF0, 0xF4, 0xF5, 0xFF, rng.randrange(256)])
+        check(bytes(b))
