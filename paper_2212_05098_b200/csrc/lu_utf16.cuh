@@ -79,6 +79,26 @@ __device__ __forceinline__ void u16_sur_masks(uint32_t x, uint32_t &hs, uint32_t
     ls = sur & lowbit;
 }
 
+// High / low bytes of the four 16-bit words of two quads, one word per byte
+// (byte j of the result = word j of the pair a, b).
+__device__ __forceinline__ uint32_t hi_bytes(uint32_t a, uint32_t b) { return prmt(a, b, 0x7531u); }
+__device__ __forceinline__ uint32_t lo_bytes(uint32_t a, uint32_t b) { return prmt(a, b, 0x6420u); }
+
+// Surrogate masks of four words from their gathered high bytes: bit 7 of
+// byte j of ls is set iff word j is a low surrogate, and bit 7 of byte j of
+// nhs is CLEAR iff word j is a high surrogate (complemented: saves a NOT).
+// The other bits are garbage; callers only test bit 7 of each byte.  4 words
+// per 32-bit op instead of 2 (u16_sur_masks): high byte in D8..DF <=>
+// surrogate, bit 2 of it tells low from high.
+__device__ __forceinline__ void u16_sur4(uint32_t hb, uint32_t &nhs, uint32_t &ls)
+{
+    const uint32_t c = hb ^ 0xD8D8D8D8u;                 // zero top 5 bits <=> surrogate
+    const uint32_t u = (c & 0x78787878u) + 0x7F7F7F7Fu;  // bit 7: some of bits 3..6 set (no carry out)
+    const uint32_t b5 = hb << 5;                         // bit 2 -> bit 7
+    nhs = u | c | b5;
+    ls = ~(u | c) & b5;
+}
+
 __device__ __forceinline__ void sts8(uint32_t addr, uint32_t v)
 {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -137,38 +157,57 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
         // error): a quad is at most 5 bytes -- the 4-byte forms of both
         // halves come from SWAR byte planes, then two byte-string selects
         if (!Boundary && sur) {
-            uint32_t hs[6], ls[6], other = 0;
+            // high / low bytes of the lane's 8 words gathered 4 per register
+            // (as K4): the class check and the 4-byte forms cover 4 words per op
+            const uint32_t hb0 = hi_bytes(w[1], w[2]), hb1 = hi_bytes(w[3], w[4]);
+            const uint32_t lb0 = lo_bytes(w[1], w[2]), lb1 = lo_bytes(w[3], w[4]);
+            uint32_t nhs0, ls0, nhs1, ls1, nhsp, lsp, nhsn, lsn;
+            u16_sur4(hb0, nhs0, ls0);
+            u16_sur4(hb1, nhs1, ls1);
+            u16_sur4(w[0] & 0xFF000000u, nhsp, lsp); // the word before the lane's words, at byte 3
+            u16_sur4(w[5] >> 8, nhsn, lsn);           // the word after them, at byte 0
+            // a BMP word >= U+0080 that is not a surrogate: (>= 0x80) & (not hs) & (not ls)
+            const uint32_t big0 = (((hb0 | (lb0 & H8)) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | hb0 | lb0;
+            const uint32_t big1 = (((hb1 | (lb1 & H8)) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | hb1 | lb1;
+            const uint32_t other = (big0 & nhs0 & ~ls0) | (big1 & nhs1 & ~ls1);
+            // pairs: ls == hs of the previous word (hs complemented)
+            const uint32_t ok = (ls0 ^ fsl(nhsp, nhs0, 8)) & (ls1 ^ fsl(nhs0, nhs1, 8)) &
+                                ((lsn ^ (nhs1 >> 24)) | 0xFFFFFF00u);
+            if (!__any_sync(0xffffffffu, ((other | ~ok) & H8) != 0)) {
+                // UTF-8 bytes of a pair led by each word (only used at high
+                // surrogates): U = (hs & 0x3FF) + 0x40 = cp >> 10, L = low 10 bits
+                //   F0 | U >> 8,  80 | (U >> 2) & 3F,  80 | (U & 3) << 4 | L >> 6,  80 | L & 3F
+                uint32_t S[8];
 #pragma unroll
-            for (int k = 0; k < 6; ++k)
-                u16_sur_masks(w[k], hs[k], ls[k]);
-            uint32_t det = 0;
-#pragma unroll
-            for (int k = 1; k <= 4; ++k) {
-                const uint32_t a = w[k] & 0xFF80FF80u;
-                const uint32_t big = (((a & 0x7FFF7FFFu) + 0x7FFF7FFFu) | a) & 0x80008000u;
-                other |= big & ~(hs[k] | ls[k]); // a BMP word >= 0x80
-            }
-#pragma unroll
-            for (int k = 1; k <= 5; ++k)
-                det |= ls[k] ^ fsl(hs[k - 1], hs[k], 16);
-            if (!__any_sync(0xffffffffu, (other | det) != 0)) {
+                for (int j = 0; j < 2; ++j) {
+                    const uint32_t hb = j ? hb1 : hb0, lb = j ? lb1 : lb0;
+                    const uint32_t hbn = j ? fsr(hb1, (w[5] >> 8) & 0xFFu, 8) : fsr(hb0, hb1, 8);
+                    const uint32_t lbn = j ? fsr(lb1, w[5] & 0xFFu, 8) : fsr(lb0, lb1, 8);
+                    const uint32_t sl = ((lb & 0x7F7F7F7Fu) + 0x40404040u) ^ (lb & H8); // low byte of U
+                    const uint32_t cy = (lb & (lb << 1) & H8) >> 7;                     // its carry (lb >= C0)
+                    const uint32_t B0 = ((hb & 0x03030303u) + cy) | 0xF0F0F0F0u;
+                    const uint32_t B1 = ((sl >> 2) & 0x3F3F3F3Fu) | H8;
+                    const uint32_t B2 = ((sl << 4) & 0x30303030u) | ((hbn << 2) & 0x0C0C0C0Cu) |
+                                        ((lbn >> 6) & 0x03030303u) | H8;
+                    const uint32_t B3 = (lbn & 0x3F3F3F3Fu) | H8;
+                    // transpose the four planes into one 4-byte string per word
+                    const uint32_t t01a = prmt(B0, B1, 0x5140u), t01b = prmt(B0, B1, 0x7362u);
+                    const uint32_t t23a = prmt(B2, B3, 0x5140u), t23b = prmt(B2, B3, 0x7362u);
+                    S[4 * j + 0] = prmt(t01a, t23a, 0x5410u);
+                    S[4 * j + 1] = prmt(t01a, t23a, 0x7632u);
+                    S[4 * j + 2] = prmt(t01b, t23b, 0x5410u);
+                    S[4 * j + 3] = prmt(t01b, t23b, 0x7632u);
+                }
                 uint32_t pl[4], ph[4], nb[4], cnt = 0;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const uint32_t x = w[k + 1];
-                    const uint32_t nx = fsr(x, w[k + 2], 16); // the word after each half
-                    const uint32_t U = (x & 0x03FF03FFu) + 0x00400040u;  // cp >> 10 of a pair led by each half
-                    const uint32_t L = nx & 0x03FF03FFu;                  // low 10 bits of the pair
-                    const uint32_t b0 = ((U >> 8) & 0x00070007u) | 0x00F000F0u;
-                    const uint32_t b1 = ((U >> 2) & 0x003F003Fu) | 0x00800080u;
-                    const uint32_t b2 = ((U << 4) & 0x00300030u) | ((L >> 6) & 0x000F000Fu) | 0x00800080u;
-                    const uint32_t b3 = (L & 0x003F003Fu) | 0x00800080u;
-                    const uint32_t p01 = prmt(b0, b1, 0x6240u), p23 = prmt(b2, b3, 0x6240u);
-                    const uint32_t e0 = prmt(p01, p23, 0x5410u), e1 = prmt(p01, p23, 0x7632u);
-                    const bool h0 = hs[k + 1] & 0x8000u, h1 = hs[k + 1] >> 31;
-                    const bool l0 = ls[k + 1] & 0x8000u, l1 = ls[k + 1] >> 31;
-                    const uint32_t t0 = h0 ? e0 : (x & 0xFFu);
-                    const uint32_t t1 = h1 ? e1 : ((x >> 16) & 0xFFu);
+                    const uint32_t nh = (k < 2 ? nhs0 : nhs1) >> (16 * (k & 1));
+                    const uint32_t lsk = (k < 2 ? ls0 : ls1) >> (16 * (k & 1));
+                    const bool h0 = !(nh & 0x80u), h1 = !(nh & 0x8000u);
+                    const bool l0 = lsk & 0x80u, l1 = lsk & 0x8000u;
+                    const uint32_t t0 = h0 ? S[2 * k] : (x & 0xFFu);
+                    const uint32_t t1 = h1 ? S[2 * k + 1] : ((x >> 16) & 0xFFu);
                     const uint32_t n0 = h0 ? 4u : (l0 ? 0u : 1u);
                     const uint32_t n1 = h1 ? 4u : (l1 ? 0u : 1u);
                     pl[k] = n0 == 4u ? t0 : (n0 == 1u ? ((t0 & 0xFFu) | (t1 << 8)) : t1);
@@ -382,26 +421,6 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
     }
 }
 
-
-// High / low bytes of the four 16-bit words of two quads, one word per byte
-// (byte j of the result = word j of the pair a, b).
-__device__ __forceinline__ uint32_t hi_bytes(uint32_t a, uint32_t b) { return prmt(a, b, 0x7531u); }
-__device__ __forceinline__ uint32_t lo_bytes(uint32_t a, uint32_t b) { return prmt(a, b, 0x6420u); }
-
-// Surrogate masks of four words from their gathered high bytes: bit 7 of
-// byte j of ls is set iff word j is a low surrogate, and bit 7 of byte j of
-// nhs is CLEAR iff word j is a high surrogate (complemented: saves a NOT).
-// The other bits are garbage; callers only test bit 7 of each byte.  4 words
-// per 32-bit op instead of 2 (u16_sur_masks): high byte in D8..DF <=>
-// surrogate, bit 2 of it tells low from high.
-__device__ __forceinline__ void u16_sur4(uint32_t hb, uint32_t &nhs, uint32_t &ls)
-{
-    const uint32_t c = hb ^ 0xD8D8D8D8u;                 // zero top 5 bits <=> surrogate
-    const uint32_t u = (c & 0x78787878u) + 0x7F7F7F7Fu;  // bit 7: some of bits 3..6 set (no carry out)
-    const uint32_t b5 = hb << 5;                         // bit 2 -> bit 7
-    nhs = u | c | b5;
-    ls = ~(u | c) & b5;
-}
 
 // K4 warp body: validate one 2 KiB chunk (1024 words) in 4 rounds of 512 B,
 // lane l holding words [8l, 8l+8) in registers.  A low surrogate must sit
