@@ -256,24 +256,31 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
             }
         }
         if (path_b) {
-            // both words of a quad as 1 or 3 bytes: three SWAR byte planes,
-            // packed into (lo, hi) with two prmt; 2, 4 or 6 bytes per quad
+            // every word 1 or 3 bytes: the three byte planes of the 3-byte
+            // form are built on the gathered high / low bytes (4 words per
+            // op); per quad two prmt pick [A0 B1_0 B2_0 A1 | B1_1 B2_1] (word 0
+            // three bytes) or [A0 A1 B1_1 B2_1]; 2, 4 or 6 bytes per quad
+            uint32_t F[2], P1[2], P2[2], big[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const uint32_t hb = hi_bytes(w[2 * j + 1], w[2 * j + 2]), lb = lo_bytes(w[2 * j + 1], w[2 * j + 2]);
+                const uint32_t z = hb | (lb & H8);
+                big[j] = (((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) & H8; // word >= 0x80: 3 bytes here
+                const uint32_t m = sgn8(big[j]);
+                const uint32_t P0 = ((hb >> 4) & 0x0F0F0F0Fu) | 0xE0E0E0E0u;                  // 1110xxxx
+                P1[j] = ((hb << 2) & 0x3C3C3C3Cu) | ((lb >> 6) & 0x03030303u) | H8;          // 10xxxxxx
+                P2[j] = (lb & 0x3F3F3F3Fu) | H8;                                            // 10xxxxxx
+                F[j] = (P0 & m) | (lb & ~m);                                                // first byte
+            }
             uint32_t pl[4], ph[4], nb[4], cnt = 0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const uint32_t x = w[k + 1];
-                const uint32_t a = x & 0xFF80FF80u;
-                const uint32_t big = (((a & 0x7FFF7FFFu) + 0x7FFF7FFFu) | a) & 0x80008000u; // 3-byte word
-                const uint32_t m = prmt(big, 0u, 0xBB99u);
-                const uint32_t b0 = ((x >> 12) & 0x000F000Fu) | 0x00E000E0u; // 1110xxxx
-                const uint32_t b1 = ((x >> 6) & 0x003F003Fu) | 0x00800080u;  // 10xxxxxx
-                const uint32_t b2 = (x & 0x003F003Fu) | 0x00800080u;         // 10xxxxxx
-                const uint32_t av = (b0 & m) | (x & ~m);                     // first byte of each word
-                const uint32_t pp = prmt(av, b1, 0x6240u);                   // [A0, B1_0, A1, B1_1]
-                // word 0 three bytes: [A0 B1_0 B2_0 A1 | B1_1 B2_1]; else [A0 A1 B1_1 B2_1]
-                pl[k] = prmt(pp, b2, (big & 0x8000u) ? 0x2410u : 0x6320u);
-                ph[k] = prmt(pp, b2, 0x0063u);
-                nb[k] = 2u + 2u * ((big >> 15 & 1u) + (big >> 31));
+                const int j = k >> 1, i0 = 2 * (k & 1);
+                const uint32_t pp = prmt(F[j], P1[j], (k & 1) ? 0x7362u : 0x5140u); // [A0, B1_0, A1, B1_1]
+                const uint32_t b0 = (big[j] >> (8 * i0 + 7)) & 1u, b1 = (big[j] >> (8 * i0 + 15)) & 1u;
+                pl[k] = prmt(pp, P2[j], b0 ? (0x2010u | ((4u + i0) << 8)) : (0x0320u | ((5u + i0) << 12)));
+                ph[k] = prmt(pp, P2[j], 0x0003u | ((5u + i0) << 4));
+                nb[k] = 2u + 2u * (b0 + b1);
                 cnt += nb[k];
             }
             const uint32_t incl = warp_incl_scan(cnt);
