@@ -146,11 +146,15 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
         w[3] = q[r].z;
         w[4] = q[r].w;
         w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : halo_n) : rn[r];
-        uint32_t any = 0;
-#pragma unroll
-        for (int k = 1; k <= 4; ++k)
-            any |= u16_any_sur(w[k]) ? 1u : 0u;
-        any |= is_ls(w[5] & 0xFFFFu) ? 1u : 0u;
+        // any surrogate among the lane's words (or a low surrogate right after
+        // them): high bytes gathered 4 words per register, D8..DF
+        uint32_t any;
+        {
+            const uint32_t c0 = hi_bytes(w[1], w[2]) ^ 0xD8D8D8D8u, c1 = hi_bytes(w[3], w[4]) ^ 0xD8D8D8D8u;
+            const uint32_t u0 = (c0 & 0x78787878u) + 0x7F7F7F7Fu, u1 = (c1 & 0x78787878u) + 0x7F7F7F7Fu;
+            any = (~(u0 | c0) | ~(u1 | c1)) & H8;
+            any |= is_ls(w[5] & 0xFFFFu) ? 1u : 0u;
+        }
         const bool sur = __any_sync(0xffffffffu, any != 0);
         // path C (warp-uniform, interior chunks): surrogates present, but every
         // word is ASCII or a surrogate and every pair is well formed (so no
@@ -244,15 +248,17 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
             path_a = !__any_sync(0xffffffffu, any800 != 0);
             if (!path_a) {
                 // path B: no 2-byte word (every word ASCII or >= U+0800)
+                // (gathered bytes, 4 words per op: >= 0x80 and not >= 0x800)
                 uint32_t two = 0;
 #pragma unroll
-                for (int k = 1; k <= 4; ++k) {
-                    const uint32_t a = w[k] & 0x07800780u, b = w[k] & 0xF800F800u;
-                    const uint32_t nza = ((a & 0x7FFF7FFFu) + 0x7FFF7FFFu) | a;
-                    const uint32_t nzb = ((b & 0x7FFF7FFFu) + 0x7FFF7FFFu) | b;
-                    two |= nza & ~nzb;
+                for (int j = 0; j < 2; ++j) {
+                    const uint32_t hb = hi_bytes(w[2 * j + 1], w[2 * j + 2]), lb = lo_bytes(w[2 * j + 1], w[2 * j + 2]);
+                    const uint32_t z = hb | (lb & H8);
+                    const uint32_t big = ((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z;
+                    const uint32_t mid = ((hb & 0x78787878u) + 0x7F7F7F7Fu) | hb;
+                    two |= big & ~mid;
                 }
-                path_b = !__any_sync(0xffffffffu, (two & 0x80008000u) != 0);
+                path_b = !__any_sync(0xffffffffu, (two & H8) != 0);
             }
         }
         if (path_b) {
