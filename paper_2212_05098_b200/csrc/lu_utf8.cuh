@@ -127,9 +127,10 @@ struct WarpResult {
 //   path 2  everything else (general detector and decoder).
 // Every path flags every bad byte its class mix can contain.
 struct U8Round {
-    uint32_t w[6]; // xp, q0..q3, xn
-    U8Masks m[5];  // masks of w[0..4] (F only computed off path 0)
-    uint32_t det;  // nonzero: a bad byte may lie in this lane's 16 bytes
+    uint32_t w[6];   // xp, q0..q3, xn
+    U8Masks m[5];    // masks of w[0..4] (F only computed off path 0)
+    uint32_t key[5]; // path 3 (fast): per byte (lead & 7) << 2 | (next >> 4) & 3 (u8_check_f), quads 1..4
+    uint32_t det;    // nonzero: a bad byte may lie in this lane's 16 bytes
     int path;
 };
 
@@ -341,7 +342,10 @@ __device__ __forceinline__ uint32_t u8_fast3(U8Round &R)
         spill = __umulhi(F, 0x01010100u);
         det |= need ^ C;
         det |= L & ~F;                                     // a 2- or 3-byte lead: not this class
-        det |= u8_check_f(x, fsr(x, R.w[k + 1], 8), U8Masks{C, L, F, F});
+        // F0 80..8F, F4 90.., F5..FF (u8_check_f); the key is kept for the decoder
+        const uint32_t key = ((x & 0x07070707u) << 2) | ((fsr(x, R.w[k + 1], 8) >> 4) & 0x03030303u);
+        det |= F & (~(key + 0x7F7F7F7Fu) | (key + 0x6F6F6F6Fu) | (x << 4));
+        R.key[k] = key;
         R.m[k].C = C;
         R.m[k].L = F;
         R.m[k].E = F;
@@ -418,16 +422,19 @@ __device__ __forceinline__ void u8_decode_quad(uint32_t x, uint32_t xn, const U8
 // surrogate) or continuations; every continuation gets the low-surrogate
 // form, which is right for the first one after a lead and never emitted for
 // the others.
-__device__ __forceinline__ void u8_decode4(uint32_t x, uint32_t xn, const U8Masks &m, uint32_t &lo, uint32_t &hi)
+__device__ __forceinline__ void u8_decode4(uint32_t x, uint32_t xn, const U8Masks &m, uint32_t key, uint32_t &lo,
+                                           uint32_t &hi)
 {
     const uint32_t n1 = fsr(x, xn, 8);
     const uint32_t n2 = fsr(x, xn, 16);
+    // low surrogate at the first continuation: DC00 | (b1 & 0xF) << 6 | b2 & 0x3F
     const uint32_t lo3 = ((n1 << 6) & 0xC0C0C0C0u) | (n2 & 0x3F3F3F3Fu);
-    const uint32_t mm = ((n1 << 2) & 0xFCFCFCFCu) | ((n2 >> 4) & 0x03030303u);
-    const uint32_t lo4 = ((mm | H8) - 0x40404040u) ^ (~mm & H8); // bytewise mm - 0x40
-    const uint32_t carry = ((n1 >> 4) | (n1 >> 5)) & 0x01010101u;
-    const uint32_t hi4 = (x & 0x07070707u) + carry + 0xD7D7D7D7u;
     const uint32_t hiS = 0xDCDCDCDCu | ((n1 >> 2) & 0x03030303u);
+    // high surrogate at the lead: (cp >> 10) - 0x40 = (key - 1) << 6 | (b1 & 0xF) << 2 | b2 >> 4 & 3,
+    // key = (b0 & 7) << 2 | b1 >> 4 & 3 >= 1 for valid leads (computed by the detector)
+    const uint32_t km1 = (key | H8) - 0x01010101u; // per byte, no borrow across bytes
+    const uint32_t hi4 = ((km1 >> 2) & 0x07070707u) | 0xD8D8D8D8u;
+    const uint32_t lo4 = ((km1 << 6) & 0xC0C0C0C0u) | ((n1 << 2) & 0x3C3C3C3Cu) | ((n2 >> 4) & 0x03030303u);
     const uint32_t sA = sgn8(x);
     const uint32_t sF = sgn8(m.F);
     lo = (x & ~sA) | (((lo4 & sF) | (lo3 & ~sF)) & sA);
@@ -574,7 +581,7 @@ __device__ __forceinline__ void u8u16_round(const U8Round &R, int r, const uint8
     } else if (P == 3) {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            u8_decode4(R.w[k + 1], R.w[k + 2], R.m[k + 1], lop[k], hip[k]);
+            u8_decode4(R.w[k + 1], R.w[k + 2], R.m[k + 1], R.key[k + 1], lop[k], hip[k]);
     } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
