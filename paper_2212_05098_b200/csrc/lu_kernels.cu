@@ -413,9 +413,9 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
 
 // ================================================================= K3 / K4
 //
-// Persistent validators fed by a TMA ring.  The input is cut into 16 KiB
-// stages (8 warp chunks of 2 KiB); CTA b takes stages b, b + grid, ...  Thread
-// 0 keeps kValStages stages in flight per CTA with cp.async.bulk (TMA bulk
+// Persistent validators fed by a TMA ring.  The input is cut into 32 KiB
+// stages (two consecutive 2 KiB chunks per warp); CTA b takes stages b,
+// b + grid, ...  Thread 0 keeps kValStages stages in flight per CTA with cp.async.bulk (TMA bulk
 // copies, completion counted on an mbarrier per ring slot), each stage copied
 // with 16 bytes of look-behind and look-ahead so every warp finds its halo
 // quads in shared memory; warps read their chunk with LDS.128.  This keeps
@@ -430,8 +430,9 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
 // The last warp to finish writes the result record.
 // ws layout: [u64 max(n - bad_pos)][u32 warps done][u32 pad][u64 count].
 
-constexpr int kValStages = 4;
-constexpr int kStageBytes = kWarps * kChunkBytes; // 16 KiB
+constexpr int kValStages = 2;
+constexpr int kValCPW = 2;                                   // chunks per warp per stage
+constexpr int kStageBytes = kWarps * kValCPW * kChunkBytes; // 32 KiB
 constexpr int kStageAlloc = kStageBytes + 32;      // + 16 B halo on each side
 constexpr size_t kSmemVal = (size_t)kValStages * kStageAlloc;
 
@@ -488,31 +489,38 @@ __global__ void __launch_bounds__(kThreads, 3) k_validate_w(const uint8_t *__res
     uint64_t i = 0, j = blockIdx.x;
     for (; j < nstages; ++i, j += gridDim.x) {
         const uint32_t slot = (uint32_t)(i % kValStages);
-        const int64_t off = (int64_t)j * kStageBytes + (int64_t)warp * kChunkBytes;
-        ChunkIn in;
         const bool fast = tma_ok(j);
         if (fast) {
             mbar_wait(bar0 + 8 * slot, (parity >> slot) & 1);
             parity ^= 1u << slot;
-            const uint8_t *sb = ring + slot * kStageAlloc + 16 + warp * kChunkBytes;
-#pragma unroll
-            for (int r = 0; r < kChunkBytes / 512; ++r) {
-                in.q[r] = *reinterpret_cast<const uint4 *>(sb + r * 512 + 16 * lane);
-                if (Swap16)
-                    in.q[r] = make_uint4(swap16x2(in.q[r].x), swap16x2(in.q[r].y), swap16x2(in.q[r].z),
-                                         swap16x2(in.q[r].w));
-            }
-            in.halo_p = *reinterpret_cast<const uint32_t *>(sb - 4);
-            in.halo_n = *reinterpret_cast<const uint32_t *>(sb + kChunkBytes);
-            if (Swap16) {
-                in.halo_p = swap16x2(in.halo_p);
-                in.halo_n = swap16x2(in.halo_n);
-            }
-        } else {
-            load_chunk<true, Swap16>(base, off, lo_b, hi_b, in);
         }
-        uint32_t err = 0, pos = 0, cc = 0;
-        if (off < hi_b) {
+        uint32_t err = 0;
+        // the warp's kValCPW consecutive chunks of the stage
+#pragma unroll 1
+        for (int ci = 0; ci < kValCPW && !err; ++ci) {
+            const int64_t off = (int64_t)j * kStageBytes + (int64_t)(warp * kValCPW + ci) * kChunkBytes;
+            if (off >= hi_b)
+                break;
+            ChunkIn in;
+            if (fast) {
+                const uint8_t *sb = ring + slot * kStageAlloc + 16 + (warp * kValCPW + ci) * kChunkBytes;
+#pragma unroll
+                for (int r = 0; r < kChunkBytes / 512; ++r) {
+                    in.q[r] = *reinterpret_cast<const uint4 *>(sb + r * 512 + 16 * lane);
+                    if (Swap16)
+                        in.q[r] = make_uint4(swap16x2(in.q[r].x), swap16x2(in.q[r].y), swap16x2(in.q[r].z),
+                                             swap16x2(in.q[r].w));
+                }
+                in.halo_p = *reinterpret_cast<const uint32_t *>(sb - 4);
+                in.halo_n = *reinterpret_cast<const uint32_t *>(sb + kChunkBytes);
+                if (Swap16) {
+                    in.halo_p = swap16x2(in.halo_p);
+                    in.halo_n = swap16x2(in.halo_n);
+                }
+            } else {
+                load_chunk<true, Swap16>(base, off, lo_b, hi_b, in);
+            }
+            uint32_t pos = 0, cc = 0;
             if (Utf16) {
                 if (fast)
                     u16val_warp_in<false, Count>(off, lo_b, hi_b, in, err, pos, &cc);
@@ -527,12 +535,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_validate_w(const uint8_t *__res
                 err = wr_s[warp].err;
                 pos = wr_s[warp].pos;
             }
-        }
-        count += cc;
-        if (err && lane == 0) {
-            const int64_t pb = off + pos - lo_b;
-            const uint64_t pu = Utf16 ? (uint64_t)(pb >> 1) : (uint64_t)pb;
-            atomicMax(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)(n - pu));
+            count += cc;
+            if (err && lane == 0) {
+                const int64_t pb = off + pos - lo_b;
+                const uint64_t pu = Utf16 ? (uint64_t)(pb >> 1) : (uint64_t)pb;
+                atomicMax(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)(n - pu));
+            }
         }
         // stop after this stage if an error is known before the next one
         bool stop_me = err != 0;
