@@ -710,7 +710,7 @@ __device__ __forceinline__ void u8val_warp_in(const uint8_t *__restrict__ base, 
                                               uint32_t warp /* warp index in tile */, uint32_t &hint,
                                               uint32_t *count = nullptr)
 {
-    uint32_t cnt = 0;
+    uint32_t cnt = 0, cacc = 0; // Count: exact total / per-byte counters (interior chunks)
     const uint32_t lane = lane_id();
     const int64_t chunk = tile_off + (int64_t)warp * kChunkBytes;
     constexpr int kRounds = kChunkBytes / 512;
@@ -742,10 +742,13 @@ __device__ __forceinline__ void u8val_warp_in(const uint8_t *__restrict__ base, 
         if (Count) {
 #pragma unroll
             for (int k = 1; k <= 4; ++k) {
-                uint32_t vm = H8;
-                if (Boundary)
-                    vm = valid_mask(chunk + r * 512 + 16 * (int64_t)lane + 4 * (k - 1), lo_b, hi_b);
-                cnt += __popc(~R.m[k].C & vm) + __popc(R.m[k].F & vm);
+                if (Boundary) {
+                    const uint32_t vm = valid_mask(chunk + r * 512 + 16 * (int64_t)lane + 4 * (k - 1), lo_b, hi_b);
+                    cnt += __popc(~R.m[k].C & vm) + __popc(R.m[k].F & vm);
+                } else {
+                    // per-byte counters (<= 2 per quad, <= 32 per chunk): no POPC
+                    cacc += ((~R.m[k].C & H8) >> 7) + (R.m[k].F >> 7);
+                }
             }
         }
         if (__any_sync(0xffffffffu, R.det != 0)) {
@@ -789,7 +792,7 @@ __device__ __forceinline__ void u8val_warp_in(const uint8_t *__restrict__ base, 
         wr.units = 0;
     }
     if (Count)
-        *count = cnt;
+        *count = cnt + ((cacc * 0x01010101u) >> 24);
 }
 
 template <bool Boundary, bool Count = false>
