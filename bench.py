@@ -429,7 +429,57 @@ def main():
             c4[name] = {"input_gib_s": round(BUF_BYTES / GIB / t, 2),
                         "frac_of_measured": round(BUF_BYTES / t / 1e9 / peak, 4), "ok": o.ok,
                         "control": "zero-error buffer"}
+        # config 4 with errors injected at 1e-6 per unit (seeds 101/102): the
+        # validators stop at the first error; the transcode writes the valid prefix
+        for name, direction, utf16, prof, seed in (("cjk_utf8_errors_1e-6", UTF8_TO_UTF16, False, "cjk", 3),
+                                                   ("emoji_utf16_errors_1e-6", UTF16_TO_UTF8, True, "emoji", 4)):
+            units = BUF_BYTES // 2 if utf16 else BUF_BYTES
+            ebuf = corpus.generate(prof, units, seed, utf16=utf16, device=dev)
+            planted = corpus.inject_errors(ebuf, utf16=utf16, rate=1e-6, seed=101 + int(utf16))
+            res = validate_device(direction, ebuf)
+            o = outcome_from_tensor(res.cpu())
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(k_ex):
+                validate_device(direction, ebuf, res=res)
+            b.record(stream)
+            torch.cuda.synchronize()
+            tv = a.elapsed_time(b) / 1e3 / k_ex
+            eout = out8 if utf16 else outs[2]
+            res, _ = transcode_device(direction, ebuf, eout)
+            ot = outcome_from_tensor(res.cpu())
+            a.record(stream)
+            for _ in range(k_ex):
+                transcode_device(direction, ebuf, eout, res=res)
+            b.record(stream)
+            torch.cuda.synchronize()
+            tt = a.elapsed_time(b) / 1e3 / k_ex
+            c4[name] = {"errors_planted": len(planted), "status": o.status.value, "first_error_unit": o.consumed,
+                        "validate_us": round(tv * 1e6, 1), "transcode_us": round(tt * 1e6, 1),
+                        "transcode_written": ot.written, "same_offset": ot.consumed == o.consumed}
+            del ebuf
         extras["config4_validate"] = c4
+        # config 1: UTF-8 -> UTF-16LE -> UTF-8 round trip of the 4 MiB mixed
+        # buffer (seed 0): two launches of a latency-bound size
+        c1src = corpus.generate("mix", 4 << 20, 0, device=dev)
+        r1, w1 = transcode_device(UTF8_TO_UTF16, c1src)
+        o1 = outcome_from_tensor(r1.cpu())
+        words = w1[: o1.written]
+        r2, b2 = transcode_device(UTF16_TO_UTF8, words)
+        o2 = outcome_from_tensor(r2.cpu())
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(k_ex):
+            transcode_device(UTF8_TO_UTF16, c1src, w1, res=r1)
+            transcode_device(UTF16_TO_UTF8, words, b2, res=r2)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t1 = a.elapsed_time(b) / 1e3 / k_ex
+        extras["config1_round_trip_4MiB"] = {"us_per_round_trip": round(t1 * 1e6, 1),
+                                             "input_gib_s": round((4 << 20) / GIB / t1, 2),
+                                             "ok": o1.ok and o2.ok and bool(torch.equal(b2[: o2.written], c1src)),
+                                             "utf16_words": o1.written}
+        del c1src, w1, b2, words
         # row 8f(4): one-pass lengths (validate + count) and char counts
         c8 = {}
         for name, op, buf in (("utf16_length_from_utf8_cjk", _native.OP_UTF16_LENGTH_FROM_UTF8, srcs[2]),

@@ -202,6 +202,32 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
         long long t_first = 0; // clock when the first tile of the window was seen
         bool partial = false;
         for (;;) {
+            // Everything in a window behind an error is "error before": publish
+            // it at once without waiting for the tiles (whose owners skip their
+            // work, see k_transcode) -- groups then never wait on them.  (The
+            // non-blocking look at the previous window's base costs nothing
+            // measurable on valid input.)
+            if (!have_base) {
+                uint32_t ready = 0;
+                if (lane == 0)
+                    ready = vtag[(w - 1) % kScanWarps] == w;
+                if (__shfl_sync(0xffffffffu, ready, 0)) {
+                    base = vbase[(w - 1) % kScanWarps];
+                    have_base = true;
+                }
+            }
+            if (have_base && (base & kErrBit)) {
+#pragma unroll
+                for (int j = 0; j < kScanPerLane; ++j)
+                    if (lane * kScanPerLane + j >= done && t0 + j < ntiles)
+                        st_release(&status[t0 + j], kFlagInc | kErrBit | (base & kValMask));
+                if (lane == 0) {
+                    vbase[w % kScanWarps] = base;
+                    __threadfence_block();
+                    vtag[w % kScanWarps] = w + 1;
+                }
+                break;
+            }
 #pragma unroll
             for (int j = 0; j < kScanPerLane; ++j)
                 if (!(have & (1u << j))) {

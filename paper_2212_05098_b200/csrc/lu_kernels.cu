@@ -180,6 +180,7 @@ struct GroupShared {
     uint32_t tile_of[2];
     uint32_t units[2]; // tile output units before its first error (or all)
     uint32_t claim;
+    uint32_t skip; // the claimed tile lies after a tile known to hold an error
 };
 
 __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n)
@@ -303,6 +304,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
 
     const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n_bytes;
     unsigned int *ticket = reinterpret_cast<unsigned int *>(status + ntiles);
+    unsigned int *err_tile = ticket + 1; // zeroed with the status words
     sel_table_init(sel);
     scan_init(scan_s);
     __syncthreads();
@@ -322,6 +324,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     uint32_t i = 0;
     uint32_t hint = 2; // K1: the warp's class-path prediction (u8_round_detect_spec)
     uint64_t st_pre = 0; // group thread 0: early poll of the next status word to resolve
+    uint32_t et_pre = 0; // group thread 0: err_tile as read before the last tile-done barrier
     // group thread 0: the next tile; the ticket is taken right after the
     // tile-done barrier so its latency overlaps the combine + publish
     uint32_t next_claim = 0;
@@ -339,16 +342,23 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
                 pipe_resolve<Dir>(ps, buf, status, res, ntiles, lo_b, n_units, st_pre);
             LU_T(12); // resolve
             ps.claim = next_claim;
+            // a tile after one that holds an error is never copied out and its
+            // count is never used: skip its work (the reference stops at the
+            // first error too).  err_tile: max(ntiles - t) over error tiles t.
+            // (et_pre was read before the last tile-done barrier: no extra L2
+            // round trip here; a stale value only means less skipping)
+            ps.skip = et_pre != 0 && ntiles - et_pre < next_claim;
             LU_T(13); // ticket wait
         }
         LU_T(0); // claim + resolve (warp 0) / nothing
         bar_sync(bar_claim, kGroupThreads); // publishes ps.claim and, for i >= 2, ps.excl[buf]
         LU_T(3); // claim barrier wait
         const uint32_t tile = ps.claim;
+        const bool skip = ps.skip;
         const int64_t tile_off = (int64_t)tile * kPipeTile;
         const bool interior = (tile_off - 4 >= lo_b) && (tile_off + kPipeTile + 4 <= hi_b);
         typename Dir::In in;
-        if (tile < ntiles) {
+        if (tile < ntiles && !skip) {
             if (interior)
                 Dir::template load<false>(base, tile_off, lo_b, hi_b, wit, in);
             else
@@ -360,7 +370,13 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
         if (tile >= ntiles)
             break;
         OutT *out_w = out_g + (buf * kGroupWarps + wit) * Dir::kStride;
-        if (interior)
+        if (skip) {
+            if (lane_id() == 0) {
+                ps.wres[buf][wit].err = 1; // "malformed": later tiles only learn that an error came before
+                ps.wres[buf][wit].pos = 0;
+                ps.wres[buf][wit].units = 0;
+            }
+        } else if (interior)
             Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in, hint);
         else
             Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in, hint);
@@ -369,6 +385,8 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
         // its L2 round trip overlaps the other warps' compute
         if (gtid == 0 && i >= 1)
             st_pre = ld_acquire(&status[ps.tile_of[buf ^ 1]]);
+        if (gtid == 0)
+            et_pre = *reinterpret_cast<volatile uint32_t *>(err_tile);
         bar_sync(bar_done, kGroupThreads);
         LU_T(5); // tile-done barrier wait
         LU_CNT(6, 1);
@@ -396,7 +414,12 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
                 ps.first_err[buf] = first;
                 ps.tile_of[buf] = tile;
                 ps.units[buf] = units;
-                st_release(&status[tile], kFlagAgg | (first < kGroupWarps ? kErrBit : 0ull) | (uint64_t)units);
+                // atomicMax: never overwrites a prefix (flag 2 > flag 1) that the
+                // scanner already published for a tile behind an error
+                atomicMax(reinterpret_cast<unsigned long long *>(&status[tile]),
+                          (unsigned long long)(kFlagAgg | (first < kGroupWarps ? kErrBit : 0ull) | (uint64_t)units));
+                if (first < kGroupWarps && !skip)
+                    atomicMax(err_tile, ntiles - tile);
             }
         }
         LU_T(7); // combine + publish
