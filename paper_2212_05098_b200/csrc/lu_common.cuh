@@ -178,12 +178,15 @@ constexpr long long kPartialAfter = 40000;           // SM cycles (~20 us)
 struct ScanShared {
     unsigned long long base[kScanWarps]; // end value of the window in the slot
     uint32_t tag[kScanWarps];            // window index + 1 once base is valid
+    uint32_t errw;                       // smallest window known to lie behind an error (~0: none)
 };
 
 __device__ __forceinline__ void scan_init(ScanShared &ss)
 {
     if (threadIdx.x < kScanWarps)
         ss.tag[threadIdx.x] = 0;
+    if (threadIdx.x == 0)
+        ss.errw = 0xffffffffu;
 }
 
 __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, uint32_t sw, ScanShared &ss)
@@ -192,6 +195,7 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
     const uint32_t nwin = (ntiles + kScanWindow - 1) / kScanWindow;
     volatile unsigned long long *vbase = ss.base;
     volatile uint32_t *vtag = ss.tag;
+    volatile uint32_t *verrw = &ss.errw;
     for (uint32_t w = sw; w < nwin; w += kScanWarps) {
         const uint32_t t0 = w * kScanWindow + lane * kScanPerLane;
         unsigned long long base = 0;
@@ -207,12 +211,16 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
             // work, see k_transcode) -- groups then never wait on them.  (The
             // non-blocking look at the previous window's base costs nothing
             // measurable on valid input.)
+            // Windows behind a window known to follow an error (errw) need no
+            // base either: the serial base hand-off would otherwise pace the
+            // publication of every remaining window.
             if (!have_base) {
                 uint32_t ready = 0;
                 if (lane == 0)
-                    ready = vtag[(w - 1) % kScanWarps] == w;
-                if (__shfl_sync(0xffffffffu, ready, 0)) {
-                    base = vbase[(w - 1) % kScanWarps];
+                    ready = (vtag[(w - 1) % kScanWarps] == w) ? 1u : (*verrw < w ? 2u : 0u);
+                ready = __shfl_sync(0xffffffffu, ready, 0);
+                if (ready) {
+                    base = ready == 1 ? vbase[(w - 1) % kScanWarps] : kErrBit;
                     have_base = true;
                 }
             }
@@ -222,6 +230,7 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                     if (lane * kScanPerLane + j >= done && t0 + j < ntiles)
                         st_release(&status[t0 + j], kFlagInc | kErrBit | (base & kValMask));
                 if (lane == 0) {
+                    atomicMin(&ss.errw, w);
                     vbase[w % kScanWarps] = base;
                     __threadfence_block();
                     vtag[w % kScanWarps] = w + 1;
@@ -290,9 +299,25 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                     ex += (uint32_t)s[j];
                 }
                 done = run;
+                if (errball && run < kScanWindow) {
+                    // the rest of the window lies behind an error: publish it now
+#pragma unroll
+                    for (int j = 0; j < kScanPerLane; ++j)
+                        if (lane * kScanPerLane + j >= run && t0 + j < ntiles)
+                            st_release(&status[t0 + j], kFlagInc | kErrBit | (base & kValMask));
+                    if (lane == 0) {
+                        atomicMin(&ss.errw, w);
+                        vbase[w % kScanWarps] = base | kErrBit;
+                        __threadfence_block();
+                        vtag[w % kScanWarps] = w + 1;
+                    }
+                    break;
+                }
                 if (run == kScanWindow) {
                     const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
                     if (lane == 0) {
+                        if (errball || (base & kErrBit))
+                            atomicMin(&ss.errw, w);
                         vbase[w % kScanWarps] = (base + wtot) | (errball ? kErrBit : 0ull);
                         __threadfence_block();
                         vtag[w % kScanWarps] = w + 1;

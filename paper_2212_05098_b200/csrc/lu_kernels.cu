@@ -367,16 +367,13 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
         if (i >= 2)
             pipe_copy<Dir>(ps, buf, wit, out_g, out_a, out_lead);
         LU_T(2); // copy-out
-        if (tile >= ntiles)
+        // past the end, or behind a known error: stop claiming (the scanner
+        // publishes everything behind an error without waiting for it); the
+        // drain below still copies out the last computed tile
+        if (tile >= ntiles || skip)
             break;
         OutT *out_w = out_g + (buf * kGroupWarps + wit) * Dir::kStride;
-        if (skip) {
-            if (lane_id() == 0) {
-                ps.wres[buf][wit].err = 1; // "malformed": later tiles only learn that an error came before
-                ps.wres[buf][wit].pos = 0;
-                ps.wres[buf][wit].units = 0;
-            }
-        } else if (interior)
+        if (interior)
             Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in, hint);
         else
             Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in, hint);
@@ -418,7 +415,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
                 // scanner already published for a tile behind an error
                 atomicMax(reinterpret_cast<unsigned long long *>(&status[tile]),
                           (unsigned long long)(kFlagAgg | (first < kGroupWarps ? kErrBit : 0ull) | (uint64_t)units));
-                if (first < kGroupWarps && !skip)
+                if (first < kGroupWarps)
                     atomicMax(err_tile, ntiles - tile);
             }
         }
