@@ -247,7 +247,7 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                 }
             // leading published run of the window: lanes before the first
             // lane with a gap are full; that lane contributes its own run
-            const uint32_t lrun = (uint32_t)__ffs(~have) - 1; // 0..4 (have < 16)
+            const uint32_t lrun = (uint32_t)__ffs(~have) - 1; // 0..kScanPerLane
             const uint32_t notfull = __ballot_sync(0xffffffffu, lrun < kScanPerLane);
             const uint32_t fl = notfull ? (uint32_t)__ffs(notfull) - 1 : 32u;
             const uint32_t myr = lane < fl ? kScanPerLane : (lane == fl ? lrun : 0u);

@@ -23,8 +23,12 @@ namespace lu {
 constexpr int kOutStrideU16 = kChunkBytes + 16;      // words per warp staging region (<= 1 word per byte)
 constexpr int kOutStrideU8 = 3 * kChunkBytes / 2 + 32; // bytes per warp region (<= 3 bytes per word)
 
-constexpr size_t kSmemK1 = 2 * sizeof(uint16_t) * kOutStrideU16 * kWarps; // 2 groups x 2 buffers x 4 warps
-constexpr size_t kSmemK2 = 2 * kOutStrideU8 * kWarps; // 2 groups x 2 buffers x 4 warps
+// staging buffers per group: K1 double-buffered (its 8.2 KiB of words per
+// warp leave no room for a third buffer at 3 CTAs/SM), K2 triple-buffered
+// (more slack for the scanner's prefix before a buffer is reused)
+constexpr int kBufsK1 = 2, kBufsK2 = 3;
+constexpr size_t kSmemK1 = kBufsK1 * sizeof(uint16_t) * kOutStrideU16 * kWarps; // 2 groups x 2 buffers x 4 warps
+constexpr size_t kSmemK2 = kBufsK2 * kOutStrideU8 * kWarps; // 2 groups x 3 buffers x 4 warps
 
 // ------------------------------------------------------------- copy-out
 
@@ -172,13 +176,15 @@ constexpr int kPipeTile = kGroupWarps * kChunkBytes; // 8 KiB
 constexpr int kPipeThreads = kGroupsPerCta * kGroupThreads;
 static_assert(kPipeThreads / 32 == kScanWarps, "CTA 0's warps are the scanner warps");
 
+constexpr int kMaxBufs = 3;
+
 struct GroupShared {
-    WarpResult wres[2][kGroupWarps];
-    uint32_t warp_excl[2][kGroupWarps];
-    uint64_t excl[2];
-    uint32_t first_err[2];
-    uint32_t tile_of[2];
-    uint32_t units[2]; // tile output units before its first error (or all)
+    WarpResult wres[kMaxBufs][kGroupWarps];
+    uint32_t warp_excl[kMaxBufs][kGroupWarps];
+    uint64_t excl[kMaxBufs];
+    uint32_t first_err[kMaxBufs];
+    uint32_t tile_of[kMaxBufs];
+    uint32_t units[kMaxBufs]; // tile output units before its first error (or all)
     uint32_t claim;
     uint32_t skip; // the claimed tile lies after a tile known to hold an error
 };
@@ -194,6 +200,7 @@ template <bool BE>
 struct DirU8U16T {
     using OutT = uint16_t;
     static constexpr int kStride = kOutStrideU16;
+    static constexpr int kBufs = kBufsK1;
     static constexpr int kUnitShift = 0; // input positions are bytes
     using In = ChunkIn;
     template <bool B>
@@ -218,6 +225,7 @@ template <bool BE>
 struct DirU16U8T {
     using OutT = uint8_t;
     static constexpr int kStride = kOutStrideU8;
+    static constexpr int kBufs = kBufsK2;
     static constexpr int kUnitShift = 1; // input positions are 16-bit words
     using In = ChunkIn;
     template <bool B>
@@ -319,7 +327,8 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     const uint32_t gtid = threadIdx.x - g * kGroupThreads;
     const uint32_t bar_claim = 1 + 3 * g, bar_done = 2 + 3 * g, bar_prefix = 3 + 3 * g;
     GroupShared &ps = gshared[g];
-    OutT *out_g = reinterpret_cast<OutT *>(smem_raw) + g * (2 * kGroupWarps * Dir::kStride);
+    constexpr uint32_t kBufs = Dir::kBufs;
+    OutT *out_g = reinterpret_cast<OutT *>(smem_raw) + g * (kBufs * kGroupWarps * Dir::kStride);
 
     uint32_t i = 0;
     uint32_t hint = 2; // K1: the warp's class-path prediction (u8_round_detect_spec)
@@ -331,14 +340,14 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     if (gtid == 0)
         next_claim = atomicAdd(ticket, 1u);
     for (;; ++i) {
-        const uint32_t buf = i & 1;
+        const uint32_t buf = i % kBufs;
         // Group thread 0 claims the next tile (atomic in flight) and resolves
         // the buffer about to be reused; one barrier publishes both.  The
         // tile's input loads are then issued before the copy-out of that
         // buffer, so the copy-out hides their latency.
         LU_T0();
         if (gtid == 0) {
-            if (i >= 2)
+            if (i >= kBufs)
                 pipe_resolve<Dir>(ps, buf, status, res, ntiles, lo_b, n_units, st_pre);
             LU_T(12); // resolve
             ps.claim = next_claim;
@@ -351,7 +360,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
             LU_T(13); // ticket wait
         }
         LU_T(0); // claim + resolve (warp 0) / nothing
-        bar_sync(bar_claim, kGroupThreads); // publishes ps.claim and, for i >= 2, ps.excl[buf]
+        bar_sync(bar_claim, kGroupThreads); // publishes ps.claim and, for i >= kBufs, ps.excl[buf]
         LU_T(3); // claim barrier wait
         const uint32_t tile = ps.claim;
         const bool skip = ps.skip;
@@ -364,7 +373,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
             else
                 Dir::template load<true>(base, tile_off, lo_b, hi_b, wit, in);
         }
-        if (i >= 2)
+        if (i >= kBufs)
             pipe_copy<Dir>(ps, buf, wit, out_g, out_a, out_lead);
         LU_T(2); // copy-out
         // past the end, or behind a known error: stop claiming (the scanner
@@ -380,8 +389,8 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
         LU_T(4); // compute
         // poll the status word resolved at the top of the next iteration now:
         // its L2 round trip overlaps the other warps' compute
-        if (gtid == 0 && i >= 1)
-            st_pre = ld_acquire(&status[ps.tile_of[buf ^ 1]]);
+        if (gtid == 0 && i + 1 >= kBufs)
+            st_pre = ld_acquire(&status[ps.tile_of[(i + 1) % kBufs]]);
         if (gtid == 0)
             et_pre = *reinterpret_cast<volatile uint32_t *>(err_tile);
         bar_sync(bar_done, kGroupThreads);
@@ -421,12 +430,15 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
         }
         LU_T(7); // combine + publish
     }
-    // drain the tile computed in the last iteration
-    if (i >= 1) {
-        if (gtid == 0)
-            pipe_resolve<Dir>(ps, (i - 1) & 1, status, res, ntiles, lo_b, n_units, 0);
-        bar_sync(bar_prefix, kGroupThreads);
-        pipe_copy<Dir>(ps, (i - 1) & 1, wit, out_g, out_a, out_lead);
+    // drain the tiles computed in the last kBufs - 1 iterations, oldest first
+    for (uint32_t d = kBufs - 1; d >= 1; --d) {
+        if (i >= d) {
+            const uint32_t b = (i - d) % kBufs;
+            if (gtid == 0)
+                pipe_resolve<Dir>(ps, b, status, res, ntiles, lo_b, n_units, 0);
+            bar_sync(bar_prefix, kGroupThreads);
+            pipe_copy<Dir>(ps, b, wit, out_g, out_a, out_lead);
+        }
     }
     LU_PROF_FLUSH();
 }
