@@ -26,8 +26,10 @@ workload, rank 0 only.
 from __future__ import annotations
 
 import argparse
+import faulthandler
 import json
 import os
+import signal
 import statistics
 import sys
 import threading
@@ -213,7 +215,13 @@ def cpu_baseline_sample():
     }
 
 
+def log(msg: str) -> None:
+    """Progress on stderr (the JSON line stays alone on stdout)."""
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
+    faulthandler.register(signal.SIGUSR1)  # `timeout -s USR1` dumps the stacks of a stuck run
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -252,6 +260,7 @@ def main():
     if reason is not None:
         raise SystemExit(f"native engine unavailable: {reason}")
 
+    log("generating config-2 inputs")
     # ---- inputs resident in HBM (each rank: its own seeded shard of profiles)
     srcs = [corpus.generate(p, BUF_BYTES, s + 100 * rank, device=dev) for p, s in PROFILES]
     outs = [torch.empty(BUF_BYTES, dtype=torch.uint16, device=dev) for _ in srcs]
@@ -275,6 +284,7 @@ def main():
             for r, g in zip(ress, gathered):
                 dist.all_gather_into_tensor(g, r)
 
+    log("warm-up")
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -283,6 +293,7 @@ def main():
     in_bytes = len(srcs) * BUF_BYTES
     out_bytes = sum(2 * o.written for o in outcomes)
 
+    log("timed region")
     # ---- timed region
     evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in srcs]
            for _ in range(args.steps)]
@@ -368,6 +379,7 @@ def main():
         "clocks": clocks.summary(),
     }
 
+    log("e2e")
     # ---- e2e through the public facade with pinned host buffers
     hosts = [s.cpu().pin_memory() for s in srcs]
     host_outs = [torch.empty(2 * BUF_BYTES, dtype=torch.uint8).pin_memory() for _ in srcs]
@@ -400,6 +412,7 @@ def main():
         k_ex = max(3, min(args.steps, 50))
         src16 = [corpus.generate(p, BUF_BYTES // 2, s + 100 * rank, utf16=True, device=dev) for p, s in PROFILES]
         out8 = torch.empty(3 * BUF_BYTES // 2, dtype=torch.uint8, device=dev)
+        log("extras: config 3")
         c3 = {}
         for (p, _), s16 in zip(PROFILES, src16):
             res, _ = transcode_device(UTF16_TO_UTF8, s16, out8)
@@ -415,6 +428,7 @@ def main():
             c3[p] = {"input_gib_s": round(BUF_BYTES / GIB / t, 2), "frac_of_measured": round(ab / t / 1e9 / peak, 4),
                      "ok": o.ok}
         extras["config3_utf16_to_utf8"] = c3
+        log("extras: config 4")
         c4 = {}
         for name, direction, buf in (("cjk_utf8", UTF8_TO_UTF16, srcs[2]), ("emoji_utf16", UTF16_TO_UTF8, src16[3])):
             res = validate_device(direction, buf)
@@ -434,6 +448,7 @@ def main():
         for name, direction, utf16, prof, seed in (("cjk_utf8_errors_1e-6", UTF8_TO_UTF16, False, "cjk", 3),
                                                    ("emoji_utf16_errors_1e-6", UTF16_TO_UTF8, True, "emoji", 4)):
             units = BUF_BYTES // 2 if utf16 else BUF_BYTES
+            log(f"extras: config 4 {name}")
             ebuf = corpus.generate(prof, units, seed, utf16=utf16, device=dev)
             planted = corpus.inject_errors(ebuf, utf16=utf16, rate=1e-6, seed=101 + int(utf16))
             res = validate_device(direction, ebuf)
@@ -461,6 +476,7 @@ def main():
         extras["config4_validate"] = c4
         # config 1: UTF-8 -> UTF-16LE -> UTF-8 round trip of the 4 MiB mixed
         # buffer (seed 0): two launches of a latency-bound size
+        log("extras: config 1")
         c1src = corpus.generate("mix", 4 << 20, 0, device=dev)
         r1, w1 = transcode_device(UTF8_TO_UTF16, c1src)
         o1 = outcome_from_tensor(r1.cpu())
@@ -481,6 +497,7 @@ def main():
                                              "utf16_words": o1.written}
         del c1src, w1, b2, words
         # row 8f(4): one-pass lengths (validate + count) and char counts
+        log("extras: lengths / counts")
         c8 = {}
         for name, op, buf in (("utf16_length_from_utf8_cjk", _native.OP_UTF16_LENGTH_FROM_UTF8, srcs[2]),
                               ("utf8_length_from_utf16le_emoji", _native.OP_UTF8_LENGTH_FROM_UTF16LE, src16[3]),
@@ -498,6 +515,7 @@ def main():
                         "frac_of_measured": round(BUF_BYTES / t / 1e9 / peak, 4)}
         extras["row8f_lengths_and_char_counts"] = c8
         # row 8f(1): UTF-16BE, swap fused into K1's compaction / K2's load
+        log("extras: UTF-16BE")
         c9 = {}
         emoji_be = src16[3].view(torch.uint8).view(-1, 2).flip(1).contiguous().view(-1)  # same text, BE
         for name, direction, buf, out in (("utf8_to_utf16be_latin", UTF8_TO_UTF16, srcs[0], outs[0]),
@@ -520,6 +538,7 @@ def main():
         tri = torch.arange(1 << 24, dtype=torch.int32, device=dev)
         tri_data = torch.stack([(tri >> 16) & 255, (tri >> 8) & 255, tri & 255], dim=1).to(torch.uint8).reshape(-1)
         tri_offs = 3 * torch.arange((1 << 24) + 1, dtype=torch.int64, device=dev)
+        log("extras: batch")
         cb = {}
         for name, vo in (("validate_utf8_all_byte_triples", True), ("utf8_to_utf16_all_byte_triples", False)):
             batch_device(UTF8_TO_UTF16, tri_data, tri_offs, validate_only=vo)
@@ -538,6 +557,7 @@ def main():
             c5 = {}
             for name, utf16 in (("utf8_to_utf16_16GiB", False), ("utf16_to_utf8_16GiB", True)):
                 units = (16 << 30) // (2 if utf16 else 1)
+                log(f"extras: config 5 {name}")
                 big = corpus.config5_generate(units, utf16=utf16, device=dev)
                 direction = UTF16_TO_UTF8 if utf16 else UTF8_TO_UTF16
                 res, bout = transcode_device(direction, big)
@@ -558,6 +578,7 @@ def main():
         line["extras"] = extras
 
     if rank == 0 and world == 1:
+        log("cpu baseline")
         try:
             line["cpu_baseline"] = cpu_baseline_sample()
         except Exception as exc:  # the baseline must not sink the GPU line

@@ -171,9 +171,15 @@ __shared__ unsigned long long s_prof[10][24]; // [warp][counter], lane 0 only
 // preceding counts, with the error bit set iff some preceding tile is
 // malformed.
 constexpr int kScanWarps = 8;
-constexpr int kScanPerLane = 4;
+#ifndef LU_SCAN_PER_LANE
+#define LU_SCAN_PER_LANE 4
+#endif
+constexpr int kScanPerLane = LU_SCAN_PER_LANE;
 constexpr uint32_t kScanWindow = 32 * kScanPerLane; // 128 tiles
-constexpr long long kPartialAfter = 40000;           // SM cycles (~20 us)
+#ifndef LU_PARTIAL_AFTER
+#define LU_PARTIAL_AFTER 40000
+#endif
+constexpr long long kPartialAfter = LU_PARTIAL_AFTER;           // SM cycles (~20 us)
 
 struct ScanShared {
     unsigned long long base[kScanWarps]; // end value of the window in the slot
@@ -264,12 +270,28 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
             if (run > done && (partial || run == kScanWindow)) {
                 LU_CNT(11, 1);
                 if (!have_base) {
+                    // Wait for the previous window's base, or for a window
+                    // before this one to be known to hold an error.  The
+                    // second exit is needed: once errw < w the previous
+                    // window's warp can publish it AND its next window
+                    // (w + 7, same slot) without waiting for anyone, so the
+                    // tag w may already be overwritten by w + 8.
                     const uint32_t slot = (w - 1) % kScanWarps;
-                    if (lane == 0)
-                        while (vtag[slot] != w)
-                            ;
-                    __syncwarp();
-                    base = vbase[slot];
+                    uint32_t ready = 0;
+                    if (lane == 0) {
+                        for (;;) {
+                            if (vtag[slot] == w) {
+                                ready = 1;
+                                break;
+                            }
+                            if (*verrw < w) {
+                                ready = 2;
+                                break;
+                            }
+                        }
+                    }
+                    ready = __shfl_sync(0xffffffffu, ready, 0);
+                    base = ready == 1 ? vbase[slot] : kErrBit;
                     have_base = true;
                 }
                 uint32_t lsum = 0, errj = kScanPerLane;

@@ -27,6 +27,13 @@ METRICS = [
     ("launch__registers_per_thread", "regs"),
     ("launch__grid_size", "grid"),
     ("smsp__inst_executed.sum", "warp_inst"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "ld_sectors"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "ld_requests"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum", "st_sectors"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_st.sum", "st_requests"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum", "sts_wavefronts"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "sts_conflicts"),
+    ("smsp__sass_inst_executed_op_shared_st.sum", "sts_inst"),
 ]
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1, "us": 1, "msecond": 1e3, "ns": 1e-3,
               "nsecond": 1e-3}
@@ -72,6 +79,10 @@ def full_rows(rep):
     return out
 
 
+def ratio(r, a, b):
+    return f"{r[a] / r[b]:.1f}" if r.get(a) is not None and r.get(b) else "-"
+
+
 def launch_shares(path):
     lines = open(path).read().splitlines()
     start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
@@ -97,13 +108,20 @@ def main():
           "Full capture (`ncu --set full --clock-control none`, tools/prof_kernels.py: 256 MiB per launch,",
           "profiles latin/cyrillic/cjk/emoji in that order for K1 and K2, then K3 on cjk and K4 on emoji).",
           "Times are ncu replay times (cold cache, serialised) -- compare shares, not absolutes.", "",
-          "| kernel | us | dram read MB | dram write MB | dram % | issue % | ALU pipe % | warps/SM | regs |",
-          "|---|---|---|---|---|---|---|---|---|"]
+          "Sectors/request: global LSU sectors per request (ideal 16 for a 16 B/thread access; the",
+          "single-lane halo/status loads and head/tail stores pull the average down; TMA bulk copies",
+          "(K3/K4) bypass these counters).  STS wf/inst: shared-store wavefronts per store instruction",
+          "(1 = conflict-free).", "",
+          "| kernel | us | dram read MB | dram write MB | dram % | issue % | ALU pipe % | warps/SM | regs "
+          "| ld sect/req | st sect/req | STS wf/inst |",
+          "|---|---|---|---|---|---|---|---|---|---|---|---|"]
     per_kernel = collections.defaultdict(list)
     for r in rows:
         md.append(f"| {r['kernel']} | {r.get('us', 0):.1f} | {r.get('dram_read', 0) / 1e6:.1f} | "
                   f"{r.get('dram_write', 0) / 1e6:.1f} | {r.get('dram_pct', 0):.1f} | {r.get('issue_pct', 0):.1f} | "
-                  f"{r.get('alu_pct', 0):.1f} | {r.get('warps_per_sm', 0):.1f} | {r.get('regs', 0):.0f} |")
+                  f"{r.get('alu_pct', 0):.1f} | {r.get('warps_per_sm', 0):.1f} | {r.get('regs', 0):.0f} | "
+                  f"{ratio(r, 'ld_sectors', 'ld_requests')} | {ratio(r, 'st_sectors', 'st_requests')} | "
+                  f"{ratio(r, 'sts_wavefronts', 'sts_inst')} |")
         per_kernel[r["kernel"]].append(r)
     tot, cnt = launch_shares(launches)
     allus = sum(tot.values())
