@@ -525,3 +525,21 @@ def test_class_switching_text(cuda_ok, utf16):
         else:
             b[pos] = rng.choice([0x80, 0xBF, 0xC0, 0xC1, 0xE0, 0xED, 0xF0, 0xF4, 0xF5, 0xFF, rng.randrange(256)])
         check(bytes(b))
+
+
+@pytest.mark.timeout(600)
+def test_error_path_progress_stress(cuda_ok):
+    """Repeated transcodes/validations of buffers with errors injected at
+    several rates never hang and always report the validator's offset
+    (tools/stress_kernels.py watches every launch).  Regression test for the
+    scanner's base hand-off behind an error (the previous window's tag slot can
+    be reused by window w + 8 before it is seen; lu_common.cuh scan_windows)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "stress_kernels.py"), "--iters", "40",
+                        "--mib", "64", "--limit-s", "20"], capture_output=True, text=True, timeout=540)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "stress ok" in r.stdout
