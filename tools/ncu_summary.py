@@ -95,6 +95,8 @@ def launch_shares(path):
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "")
         us = v / 1e3 if unit in ("nsecond", "ns") else v * (1e3 if unit in ("msecond", "ms") else 1)
+        if "lu::" not in r["Kernel Name"]:
+            continue  # torch kernels of the seeded input generator (set-up, outside the step)
         k = short(r["Kernel Name"])
         tot[k] += us
         cnt[k] += 1
@@ -126,7 +128,9 @@ def main():
     tot, cnt = launch_shares(launches)
     allus = sum(tot.values())
     md += ["", "Launch list of `python bench.py --steps 2 --warmup 3 --no-extras --e2e-steps 1`",
-           "(`ncu --metrics gpu__time_duration.sum --clock-control none`):", "",
+           "(`ncu --metrics gpu__time_duration.sum --clock-control none`; this package's kernels only -- the",
+           "torch kernels of the input generator run before the timed step; the per-call status-word",
+           "memset is a driver memset, not a kernel):", "",
            "| kernel | launches | total us | share |", "|---|---|---|---|"]
     for k, v in tot.most_common():
         md.append(f"| {k} | {cnt[k]} | {v:.1f} | {100 * v / allus:.1f}% |")
