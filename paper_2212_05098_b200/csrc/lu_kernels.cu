@@ -106,19 +106,34 @@ __device__ __forceinline__ void copy_out_u8(const uint8_t *src, uint32_t cnt, ui
     uint8_t *dst = out_a + (g0 - shift);
     const uint32_t total = shift + cnt;
     const uint32_t full_lo = shift ? 1u : 0u, full_hi = total >> 4;
-    const uint32_t *s32 = reinterpret_cast<const uint32_t *>(src);
-    const uint32_t sh = 8u * ((16u - shift) & 3u);
-    if (sh == 0) {
-        for (uint32_t c = full_lo + lane; c < full_hi; c += 32) {
-            const uint32_t m = (16 * c - shift) >> 2;
-            __stcs(reinterpret_cast<uint4 *>(dst) + c, make_uint4(s32[m], s32[m + 1], s32[m + 2], s32[m + 3]));
-        }
+    // Output chunk c holds staging bytes [16c - shift, +16): for shift > 0
+    // that is byte r = 16 - shift of staging vector c - 1 onwards.  Read the
+    // two aligned vectors with conflict-free LDS.128 (5 LDS.32 per chunk were
+    // 4-way bank conflicted) and funnel-shift by the warp-uniform word offset
+    // q = r / 4 (one specialised loop per value) and byte shift sh.
+    const uint4 *s128 = reinterpret_cast<const uint4 *>(src);
+    uint4 *d128 = reinterpret_cast<uint4 *>(dst);
+    if (shift == 0) {
+#pragma unroll 1
+        for (uint32_t c = lane; c < full_hi; c += 32)
+            __stcs(d128 + c, s128[c]);
     } else {
-        for (uint32_t c = full_lo + lane; c < full_hi; c += 32) {
-            const uint32_t m = (16 * c - shift) >> 2;
-            const uint32_t w0 = s32[m], w1 = s32[m + 1], w2 = s32[m + 2], w3 = s32[m + 3], w4 = s32[m + 4];
-            __stcs(reinterpret_cast<uint4 *>(dst) + c,
-                   make_uint4(fsr(w0, w1, sh), fsr(w1, w2, sh), fsr(w2, w3, sh), fsr(w3, w4, sh)));
+        const uint32_t r = 16u - shift, sh = 8u * (r & 3u);
+        switch (r >> 2) {
+#define LU_COPY8_CASE(Q, BODY)                                                                                         \
+    case Q:                                                                                                            \
+        _Pragma("unroll 1") for (uint32_t c = full_lo + lane; c < full_hi; c += 32) {                                  \
+            const uint4 a = s128[c - 1], b = s128[c];                                                                  \
+            const uint32_t w0 = a.x, w1 = a.y, w2 = a.z, w3 = a.w, w4 = b.x, w5 = b.y, w6 = b.z, w7 = b.w;             \
+            (void)w0, (void)w1, (void)w2, (void)w3, (void)w4, (void)w5, (void)w6, (void)w7;                            \
+            __stcs(d128 + c, BODY);                                                                                    \
+        }                                                                                                              \
+        break;
+            LU_COPY8_CASE(0, make_uint4(fsr(w0, w1, sh), fsr(w1, w2, sh), fsr(w2, w3, sh), fsr(w3, w4, sh)))
+            LU_COPY8_CASE(1, make_uint4(fsr(w1, w2, sh), fsr(w2, w3, sh), fsr(w3, w4, sh), fsr(w4, w5, sh)))
+            LU_COPY8_CASE(2, make_uint4(fsr(w2, w3, sh), fsr(w3, w4, sh), fsr(w4, w5, sh), fsr(w5, w6, sh)))
+            LU_COPY8_CASE(3, make_uint4(fsr(w3, w4, sh), fsr(w4, w5, sh), fsr(w5, w6, sh), fsr(w6, w7, sh)))
+#undef LU_COPY8_CASE
         }
     }
     uint32_t chunk;
