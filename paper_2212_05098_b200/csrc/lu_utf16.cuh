@@ -111,6 +111,19 @@ __device__ __forceinline__ void sts8_if(uint32_t addr, uint32_t v, uint32_t n, u
                  : "memory");
 }
 
+// 16-bit stores of two UTF-8 bytes (low half of v) at an even address
+__device__ __forceinline__ void sts16b(uint32_t addr, uint32_t v)
+{
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+}
+
+__device__ __forceinline__ void sts16b_if(uint32_t addr, uint32_t v, uint32_t n, uint32_t j)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.gt.u32 p, %2, %3;\n\t@p st.shared.u16 [%0], %1;\n\t}" ::"r"(addr),
+                 "h"((unsigned short)v), "r"(n), "r"(j)
+                 : "memory");
+}
+
 // K2 warp body for the pipelined kernel: the warp's 2 KiB chunk (1024 words)
 // in 4 rounds of 512 B, lane l holding words [8l, 8l+8) of the round in
 // registers; neighbour words by shuffle.  Per word: pair-aware UTF-8 encode
@@ -291,16 +304,29 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
             }
             const uint32_t incl = warp_incl_scan(cnt);
             uint32_t off = running + incl - cnt;
+            // every quad is 2, 4 or 6 bytes, so all stores of the round share
+            // the parity of the warp's running offset (warp-uniform): even --
+            // three exact 16-bit stores; odd -- the first and last byte alone,
+            // the pairs between them 16-bit (was six 8-bit stores per quad)
+            if (!(running & 1u)) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t a = sbase + off;
-                sts8(a, pl[k]);
-                sts8(a + 1, pl[k] >> 8);
-                sts8_if(a + 2, pl[k] >> 16, nb[k], 2);
-                sts8_if(a + 3, pl[k] >> 24, nb[k], 3);
-                sts8_if(a + 4, ph[k], nb[k], 4);
-                sts8_if(a + 5, ph[k] >> 8, nb[k], 5);
-                off += nb[k];
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t a = sbase + off;
+                    sts16b(a, pl[k]);
+                    sts16b_if(a + 2, pl[k] >> 16, nb[k], 2);
+                    sts16b_if(a + 4, ph[k], nb[k], 4);
+                    off += nb[k];
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t a = sbase + off;
+                    sts8(a, pl[k]);
+                    sts16b_if(a + 1, pl[k] >> 8, nb[k], 3);
+                    sts16b_if(a + 3, fsr(pl[k], ph[k], 24), nb[k], 5);
+                    sts8(a + nb[k] - 1, prmt(pl[k], ph[k], nb[k] - 1));
+                    off += nb[k];
+                }
             }
             running += __shfl_sync(0xffffffffu, incl, 31);
             continue;
