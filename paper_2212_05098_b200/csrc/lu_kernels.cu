@@ -163,6 +163,24 @@ __device__ __forceinline__ void sel_table_init(SelPair *sel)
         }
         sel[idx].s01 = s[0];
         sel[idx].s23 = s[1];
+    } else if (threadIdx.x < 32) {
+        // K2 path C (u16u8_warp_r): entry (c0 | c1 << 2) for the classes of a
+        // word pair (0 ASCII, 1 low surrogate, 2 high surrogate; T0 / T1 =
+        // their 4-byte strings, bytes 0-3 / 4-7 of prmt): s01 = selector of
+        // the first four bytes, s23 = selector of the fifth | byte count << 16.
+        // Pairs that cannot occur in a path-C round (AL, LL, HA, HH) emit 0.
+        const uint32_t idx = threadIdx.x - 16;
+        uint32_t lo = 0, hi = 0, nb = 0;
+        switch (idx) {
+        case 0: lo = 0x0040u; nb = 2; break;             // A A
+        case 8: lo = 0x6540u; hi = 0x7u; nb = 5; break;  // A H
+        case 1: lo = 0x0004u; nb = 1; break;             // L A
+        case 9: lo = 0x7654u; nb = 4; break;             // L H
+        case 6: lo = 0x3210u; nb = 4; break;             // H L
+        default: break;
+        }
+        sel[16 + idx].s01 = lo;
+        sel[16 + idx].s23 = hi | (nb << 16);
     }
 }
 
@@ -251,9 +269,9 @@ struct DirU16U8T {
     }
     template <bool B>
     __device__ static void compute(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, OutT *out_w,
-                                   const SelPair *, WarpResult &wr, uint32_t wit, const In &in, uint32_t &)
+                                   const SelPair *sel, WarpResult &wr, uint32_t wit, const In &in, uint32_t &)
     {
-        u16u8_warp_r<B>(base, tile_off, lo_b, hi_b, out_w, wr, wit, in);
+        u16u8_warp_r<B>(base, tile_off, lo_b, hi_b, out_w, sel + 16, wr, wit, in);
     }
     __device__ static void copy_out(const OutT *src, uint32_t cnt, OutT *out_a, uint64_t g0)
     {
@@ -321,7 +339,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
 {
     using OutT = typename Dir::OutT;
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    __shared__ SelPair sel[16];
+    __shared__ SelPair sel[32]; // K1 compaction selectors, then K2 path-C selectors
     __shared__ GroupShared gshared[kGroupsPerCta];
     __shared__ ScanShared scan_s;
 
@@ -656,10 +674,9 @@ __global__ void __launch_bounds__(kThreads) k_batch(const uint8_t *__restrict__ 
     constexpr bool kUtf16 = (Op == 1 || Op == 3);
     constexpr int kShift = kUtf16 ? 1 : 0;
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    __shared__ SelPair sel[16];
+    __shared__ SelPair sel[32];
     __shared__ WarpResult wres[kWarps];
-    if (Op == 0)
-        sel_table_init(sel);
+    sel_table_init(sel);
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
@@ -684,7 +701,7 @@ __global__ void __launch_bounds__(kThreads) k_batch(const uint8_t *__restrict__ 
                     copy_out_u16(stage, units, reinterpret_cast<uint16_t *>(out_a), out_lead + u0 + running);
                 } else {
                     uint8_t *stage = smem_raw + warp * kOutStrideU8;
-                    u16u8_warp_r<true>(base, chunk, lo_b, hi_b, stage, wres[warp], 0, in);
+                    u16u8_warp_r<true>(base, chunk, lo_b, hi_b, stage, sel + 16, wres[warp], 0, in);
                     __syncwarp();
                     units = wres[warp].units;
                     copy_out_u8(stage, units, reinterpret_cast<uint8_t *>(out_a), out_lead + 3 * u0 + running);

@@ -131,8 +131,8 @@ __device__ __forceinline__ void sts16b_if(uint32_t addr, uint32_t v, uint32_t n,
 // fast path skips the surrogate logic when a round has no surrogate.
 template <bool Boundary>
 __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
-                                             int64_t hi_b, uint8_t *out_w, WarpResult &wr, uint32_t warp,
-                                             const ChunkIn &in)
+                                             int64_t hi_b, uint8_t *out_w, const SelPair *sel, WarpResult &wr,
+                                             uint32_t warp, const ChunkIn &in)
 {
     const uint32_t lane = lane_id();
     const int64_t chunk = tile_off + (int64_t)warp * kChunkBytes;
@@ -202,7 +202,10 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
                     const uint32_t lbn = j ? fsr(lb1, w[5] & 0xFFu, 8) : fsr(lb0, lb1, 8);
                     const uint32_t sl = ((lb & 0x7F7F7F7Fu) + 0x40404040u) ^ (lb & H8); // low byte of U
                     const uint32_t cy = (lb & (lb << 1) & H8) >> 7;                     // its carry (lb >= C0)
-                    const uint32_t B0 = ((hb & 0x03030303u) + cy) | 0xF0F0F0F0u;
+                    // byte 0 of a non-high-surrogate word's string: its low
+                    // byte (the ASCII character; unused for a low surrogate)
+                    const uint32_t nm = sgn8(j ? nhs1 : nhs0);
+                    const uint32_t B0 = (lb & nm) | ((((hb & 0x03030303u) + cy) | 0xF0F0F0F0u) & ~nm);
                     const uint32_t B1 = ((sl >> 2) & 0x3F3F3F3Fu) | H8;
                     const uint32_t B2 = ((sl << 4) & 0x30303030u) | ((hbn << 2) & 0x0C0C0C0Cu) |
                                         ((lbn >> 6) & 0x03030303u) | H8;
@@ -215,21 +218,25 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
                     S[4 * j + 2] = prmt(t01b, t23b, 0x5410u);
                     S[4 * j + 3] = prmt(t01b, t23b, 0x7632u);
                 }
+                // per word pair: class index (bit 7 of a byte = high
+                // surrogate, bit 6 = low surrogate; c = 2 H, 1 L, 0 ASCII) ->
+                // selector table: the pair's bytes are one prmt of the two
+                // 4-byte strings, plus a fifth byte (A H) and the count
+                const uint32_t cl0 = (~nhs0 & H8) | ((ls0 & H8) >> 1);
+                const uint32_t cl1 = (~nhs1 & H8) | ((ls1 & H8) >> 1);
+                const char *selb = reinterpret_cast<const char *>(sel);
                 uint32_t pl[4], ph[4], nb[4], cnt = 0;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const uint32_t x = w[k + 1];
-                    const uint32_t nh = (k < 2 ? nhs0 : nhs1) >> (16 * (k & 1));
-                    const uint32_t lsk = (k < 2 ? ls0 : ls1) >> (16 * (k & 1));
-                    const bool h0 = !(nh & 0x80u), h1 = !(nh & 0x8000u);
-                    const bool l0 = lsk & 0x80u, l1 = lsk & 0x8000u;
-                    const uint32_t t0 = h0 ? S[2 * k] : (x & 0xFFu);
-                    const uint32_t t1 = h1 ? S[2 * k + 1] : ((x >> 16) & 0xFFu);
-                    const uint32_t n0 = h0 ? 4u : (l0 ? 0u : 1u);
-                    const uint32_t n1 = h1 ? 4u : (l1 ? 0u : 1u);
-                    pl[k] = n0 == 4u ? t0 : (n0 == 1u ? ((t0 & 0xFFu) | (t1 << 8)) : t1);
-                    ph[k] = n0 == 4u ? t1 : (n0 == 1u ? (t1 >> 24) : 0u);
-                    nb[k] = n0 + n1;
+                    const uint32_t cl = k < 2 ? cl0 : cl1;
+                    // byte offset (idx * 8) of idx = c0 | c1 << 2: bits 6, 7, 14, 15
+                    // (or 22, 23, 30, 31) of cl moved to bits 3..6 by a multiply
+                    const uint32_t bo = (k & 1) ? (__umulhi(cl & 0xC0C00000u, 0x2080u) & 0x78u)
+                                                : (__umulhi(cl & 0x0000C0C0u, 0x20800000u) & 0x78u);
+                    const SelPair sp = *reinterpret_cast<const SelPair *>(selb + bo);
+                    pl[k] = prmt(S[2 * k], S[2 * k + 1], sp.s01);
+                    ph[k] = prmt(S[2 * k], S[2 * k + 1], sp.s23);
+                    nb[k] = sp.s23 >> 16;
                     cnt += nb[k];
                 }
                 const uint32_t incl = warp_incl_scan(cnt);
