@@ -181,6 +181,22 @@ __device__ __forceinline__ void sel_table_init(SelPair *sel)
         }
         sel[16 + idx].s01 = lo;
         sel[16 + idx].s23 = hi | (nb << 16);
+    } else if (threadIdx.x < 40) {
+        // K2 path A: entry (odd << 2 | big1 << 1 | big0) for a word pair of
+        // 1- or 2-byte words (big = 2-byte); F / S = planes of the first /
+        // second bytes of 4 words (bytes 0-3 / 4-7 of prmt), the pair being
+        // words 0, 1 (odd = 0) or 2, 3 (odd = 1) of the planes
+        const uint32_t idx = threadIdx.x - 32;
+        const uint32_t o = 2u * (idx >> 2), b0 = idx & 1u, b1 = (idx >> 1) & 1u;
+        uint32_t sel_v = 0, j = 0;
+        const uint32_t bytes[4] = {o, 4u + o, o + 1u, 5u + o}; // F0 S0 F1 S1
+        for (uint32_t t = 0; t < 4; ++t) {
+            if ((t == 1 && !b0) || (t == 3 && !b1))
+                continue;
+            sel_v |= bytes[t] << (4 * j++);
+        }
+        sel[32 + idx].s01 = sel_v;
+        sel[32 + idx].s23 = j; // byte count
     }
 }
 
@@ -339,7 +355,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
 {
     using OutT = typename Dir::OutT;
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    __shared__ SelPair sel[32]; // K1 compaction selectors, then K2 path-C selectors
+    __shared__ SelPair sel[40]; // K1 compaction selectors, then K2 path-C and path-A selectors
     __shared__ GroupShared gshared[kGroupsPerCta];
     __shared__ ScanShared scan_s;
 
@@ -674,7 +690,7 @@ __global__ void __launch_bounds__(kThreads) k_batch(const uint8_t *__restrict__ 
     constexpr bool kUtf16 = (Op == 1 || Op == 3);
     constexpr int kShift = kUtf16 ? 1 : 0;
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    __shared__ SelPair sel[32];
+    __shared__ SelPair sel[40];
     __shared__ WarpResult wres[kWarps];
     sel_table_init(sel);
     __syncthreads();

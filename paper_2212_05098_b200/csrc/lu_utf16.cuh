@@ -341,19 +341,33 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
         if (path_a) {
             // self-contained (own scan and stores): its live ranges do not
             // overlap the general path's, which otherwise spills
+            // first / second byte planes of 4 words per op on the gathered
+            // high / low bytes (high byte <= 7 here): F = lb (ASCII) or
+            // 110 hhh ll, S = 10 llllll; per word pair one prmt selected by
+            // the pair's 2-byte flags (table after path C's, K2 sel + 16)
+            uint32_t F[2], S[2], big[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const uint32_t hb = hi_bytes(w[2 * j + 1], w[2 * j + 2]), lb = lo_bytes(w[2 * j + 1], w[2 * j + 2]);
+                const uint32_t z = hb | (lb & H8);
+                big[j] = (((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) & H8; // word >= 0x80
+                const uint32_t m = sgn8(big[j]);
+                const uint32_t f2 = (hb << 2) | ((lb >> 6) & 0x03030303u) | 0xC0C0C0C0u;
+                F[j] = (f2 & m) | (lb & ~m);
+                S[j] = (lb & 0x3F3F3F3Fu) | H8;
+            }
+            const char *selb = reinterpret_cast<const char *>(sel) + 128;
             uint32_t pk[4], nb[4], cnt = 0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const uint32_t x = w[k + 1];
-                const uint32_t a = x & 0xFF80FF80u;
-                const uint32_t big = (((a & 0x7FFF7FFFu) + 0x7FFF7FFFu) | a) & 0x80008000u; // word >= 0x80
-                // both halves as 2-byte forms: 110xxxxx 10xxxxxx
-                const uint32_t e2 = ((x >> 6) & 0x001F001Fu) | ((x << 8) & 0x3F003F00u) | 0x80C080C0u;
-                const uint32_t m = prmt(big, 0u, 0xBB99u); // 0xFFFF in each half with a 2-byte word
-                const uint32_t v = (e2 & m) | (x & ~m);     // per half: its 1 or 2 bytes
-                // pack: drop the empty high byte of a 1-byte low word
-                pk[k] = prmt(v, v, (big & 0x8000u) ? 0x3210u : 0x3320u);
-                nb[k] = 2u + (big >> 15 & 1u) + (big >> 31);
+                const uint32_t bg = big[k >> 1];
+                // byte offset (idx * 8) of idx = big0 | big1 << 1: bits 7, 15 (or
+                // 23, 31) of the plane moved to bits 3, 4 by a multiply
+                const uint32_t bo = (k & 1) ? 32u + (__umulhi(bg & 0x80800000u, 0x1020u) & 0x18u)
+                                            : (__umulhi(bg & 0x00008080u, 0x10200000u) & 0x18u);
+                const SelPair sp = *reinterpret_cast<const SelPair *>(selb + bo);
+                pk[k] = prmt(F[k >> 1], S[k >> 1], sp.s01);
+                nb[k] = sp.s23;
                 cnt += nb[k];
             }
             const uint32_t incl = warp_incl_scan(cnt);
