@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--iters", type=int, default=40)
     ap.add_argument("--mib", type=int, default=64)
     ap.add_argument("--limit-s", type=float, default=10.0)
+    ap.add_argument("--random-iters", type=int, default=200)
+    ap.add_argument("--seed", type=int, default=1)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     stream = torch.cuda.current_stream(dev)
@@ -66,6 +68,48 @@ def main():
                 launches += 2
                 assert to.consumed == vo.consumed and to.status == vo.status, (what, to, vo)
             del buf
+    # random sizes / misalignment / a single error near a tile or window
+    # boundary (8 KiB tiles, 128-tile scanner windows = 1 MiB)
+    import random
+
+    rng = random.Random(args.seed)
+    base8 = corpus.generate("mix", n + 64, 77, device=dev)
+    base16 = corpus.generate("mix", n // 2 + 64, 78, utf16=True, device=dev)
+    for it in range(args.random_iters):
+        utf16 = bool(it & 1)
+        units = rng.choice([1, 7, 100, 4096, 65536, 1 << 20, (1 << 20) + 3, rng.randrange(1, n // 2 if utf16 else n)])
+        lead = rng.randrange(0, 16)
+        # a view at an odd offset: misaligned input pointers (the kernels
+        # address a 16-byte aligned frame with a lead offset)
+        if utf16:
+            buf = base16[2 * lead: 2 * (lead + units)]
+        else:
+            buf = base8[lead: lead + units]
+        # buf itself is valid only if the cut is on character boundaries;
+        # either way the kernels must finish and agree with the validator
+        restore = None
+        if rng.random() < 0.7 and units > 16:
+            tile_units = 8192 // (2 if utf16 else 1)
+            k = rng.randrange(0, max(1, units // tile_units))
+            pos = min(units - 1, max(0, k * tile_units + rng.randrange(-3, 4)))
+            if utf16:
+                restore = (buf.view(torch.int16), pos, buf.view(torch.int16)[pos].clone())
+                buf.view(torch.int16)[pos] = torch.tensor(0xDC00 - 65536, dtype=torch.int16)
+            else:
+                restore = (buf, pos, buf[pos].clone())
+                buf[pos] = 0xFF
+        direction = UTF16_TO_UTF8 if utf16 else UTF8_TO_UTF16
+        what = f"random iter {it} units={units} lead={lead} utf16={utf16}"
+        vres = validate_device(direction, buf)
+        wait(stream, args.limit_s, "validate " + what)
+        vo = outcome_from_tensor(vres.cpu())
+        tres, _ = transcode_device(direction, buf)
+        wait(stream, args.limit_s, "transcode " + what)
+        to = outcome_from_tensor(tres.cpu())
+        launches += 2
+        assert to.consumed == vo.consumed and to.status == vo.status, (what, to, vo)
+        if restore is not None:
+            restore[0][restore[1]] = restore[2]
     print(f"stress ok: {launches} launches in {time.time() - t0:.1f} s", flush=True)
 
 
