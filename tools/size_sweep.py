@@ -1,3 +1,6 @@
+"""K1 time per launch vs input size (latin, 1 MiB .. 1 GiB) and a torch
+zero_ of the workspace: the fixed per-launch cost is the intercept.
+usage: python tools/size_sweep.py"""
 import os, sys, torch
 sys.path.insert(0, os.getcwd())
 from paper_2212_05098_b200 import UTF8_TO_UTF16, _native, corpus, transcode_device
