@@ -356,7 +356,8 @@ __device__ __forceinline__ uint32_t u8_fast3(U8Round &R)
 
 // Round detection with the warp's path prediction (see above); hint is
 // warp-uniform, updated to the round's actual path on a miss.
-__device__ __forceinline__ void u8_round_detect_spec(U8Round &R, uint32_t &hint)
+// Returns true when the prediction held (R.det = 0).
+__device__ __forceinline__ bool u8_round_detect_spec(U8Round &R, uint32_t &hint)
 {
     uint32_t fd;
     switch (hint) {
@@ -376,10 +377,11 @@ __device__ __forceinline__ void u8_round_detect_spec(U8Round &R, uint32_t &hint)
     if (__any_sync(0xffffffffu, fd != 0)) {
         u8_round_detect(R);
         hint = (uint32_t)R.path;
-    } else {
-        R.path = (int)hint;
-        R.det = 0;
+        return false;
     }
+    R.path = (int)hint;
+    R.det = 0;
+    return true;
 }
 
 // ============================================================ K1: utf8->utf16
@@ -503,7 +505,9 @@ __device__ __forceinline__ void u8u16_round(const U8Round &R, int r, const uint8
     const uint32_t excl = incl - cnt;
     const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
 
-    if (__any_sync(0xffffffffu, R.det != 0)) {
+    // a predicted (fast) round has det = 0 except lane 31's chunk-end check
+    // in the chunk's last round: no vote needed in its other rounds
+    if ((P == 2 || r == kChunkBytes / 512 - 1) && __any_sync(0xffffffffu, R.det != 0)) {
         // exact resolution in stream order: tail of the previous round first
         const int64_t rstart = chunk + r * 512;
         bool found = false;
@@ -733,7 +737,7 @@ __device__ __forceinline__ void u8val_warp_in(const uint8_t *__restrict__ base, 
         R.w[3] = q[r].z;
         R.w[4] = q[r].w;
         R.w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : halo_n) : rn[r];
-        u8_round_detect_spec(R, hint);
+        const bool predicted = u8_round_detect_spec(R, hint);
         if (r == kRounds - 1 && lane == 31) {
             const uint32_t cn = u8_classify(R.w[5]).C;
             const U8Masks &m = R.m[4];
@@ -751,7 +755,8 @@ __device__ __forceinline__ void u8val_warp_in(const uint8_t *__restrict__ base, 
                 }
             }
         }
-        if (__any_sync(0xffffffffu, R.det != 0)) {
+        // a predicted round has det = 0 except the chunk-end check (last round)
+        if ((!predicted || r == kRounds - 1) && __any_sync(0xffffffffu, R.det != 0)) {
             const int64_t rstart = chunk + r * 512;
             uint32_t tb = 3;
             if (r > 0 && lane == 0) {
