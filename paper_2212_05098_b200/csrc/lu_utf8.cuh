@@ -356,8 +356,11 @@ __device__ __forceinline__ uint32_t u8_fast3(U8Round &R)
 
 // Round detection with the warp's path prediction (see above); hint is
 // warp-uniform, updated to the round's actual path on a miss.
-// Returns true when the prediction held (R.det = 0).
-__device__ __forceinline__ bool u8_round_detect_spec(U8Round &R, uint32_t &hint)
+// Returns true when the prediction held (R.det = 0).  check_end (lane 31 in
+// the chunk's last round): the chunk-end check joins the prediction vote, so a
+// predicted round never needs the resolution vote; on a miss the caller adds
+// it to R.det.
+__device__ __forceinline__ bool u8_round_detect_spec(U8Round &R, uint32_t &hint, bool check_end = false)
 {
     uint32_t fd;
     switch (hint) {
@@ -374,6 +377,8 @@ __device__ __forceinline__ bool u8_round_detect_spec(U8Round &R, uint32_t &hint)
         fd = 1;
         break;
     }
+    if (check_end)
+        fd |= u8_chunk_end_check(R);
     if (__any_sync(0xffffffffu, fd != 0)) {
         u8_round_detect(R);
         hint = (uint32_t)R.path;
@@ -505,9 +510,9 @@ __device__ __forceinline__ void u8u16_round(const U8Round &R, int r, const uint8
     const uint32_t excl = incl - cnt;
     const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
 
-    // a predicted (fast) round has det = 0 except lane 31's chunk-end check
-    // in the chunk's last round: no vote needed in its other rounds
-    if ((P == 2 || r == kChunkBytes / 512 - 1) && __any_sync(0xffffffffu, R.det != 0)) {
+    // a predicted (fast) round has det = 0 (lane 31's chunk-end check joined
+    // the prediction vote): no resolution vote
+    if (P == 2 && __any_sync(0xffffffffu, R.det != 0)) {
         // exact resolution in stream order: tail of the previous round first
         const int64_t rstart = chunk + r * 512;
         bool found = false;
@@ -669,11 +674,13 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
         bool fast = false;
 #define LU_FAST_ROUND(PP, FN)                                                                                          \
     if (hint == PP) {                                                                                                  \
-        const uint32_t fd = FN(R);                                                                                     \
+        uint32_t fd = FN(R);                                                                                           \
+        if (r == kRounds - 1 && lane == 31)                                                                            \
+            fd |= u8_chunk_end_check(R); /* joins the prediction vote: det = 0 below */                                \
         if (!__any_sync(0xffffffffu, fd != 0)) {                                                                       \
             fast = true;                                                                                               \
             R.path = PP;                                                                                               \
-            R.det = (r == kRounds - 1 && lane == 31) ? u8_chunk_end_check(R) : 0u;                                     \
+            R.det = 0u;                                                                                                \
             u8u16_round<PP, Boundary, BE>(R, r, base, tile_off, chunk, lane_off, lo_b, hi_b, sbase, sel, running, err, \
                                           err_pos, units);                                                             \
         }                                                                                                              \
@@ -737,12 +744,10 @@ __device__ __forceinline__ void u8val_warp_in(const uint8_t *__restrict__ base, 
         R.w[3] = q[r].z;
         R.w[4] = q[r].w;
         R.w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : halo_n) : rn[r];
-        const bool predicted = u8_round_detect_spec(R, hint);
-        if (r == kRounds - 1 && lane == 31) {
-            const uint32_t cn = u8_classify(R.w[5]).C;
-            const U8Masks &m = R.m[4];
-            R.det |= (m.L & ~fsr(m.C, cn, 8)) | (m.E & ~fsr(m.C, cn, 16)) | (m.F & ~fsr(m.C, cn, 24));
-        }
+        const bool last31 = r == kRounds - 1 && lane == 31;
+        const bool predicted = u8_round_detect_spec(R, hint, last31);
+        if (!predicted && last31)
+            R.det |= u8_chunk_end_check(R);
         if (Count) {
 #pragma unroll
             for (int k = 1; k <= 4; ++k) {
@@ -755,8 +760,8 @@ __device__ __forceinline__ void u8val_warp_in(const uint8_t *__restrict__ base, 
                 }
             }
         }
-        // a predicted round has det = 0 except the chunk-end check (last round)
-        if ((!predicted || r == kRounds - 1) && __any_sync(0xffffffffu, R.det != 0)) {
+        // a predicted round has det = 0 (its chunk-end check joined the prediction vote)
+        if (!predicted && __any_sync(0xffffffffu, R.det != 0)) {
             const int64_t rstart = chunk + r * 512;
             uint32_t tb = 3;
             if (r > 0 && lane == 0) {
