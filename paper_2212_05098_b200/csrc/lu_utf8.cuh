@@ -695,9 +695,9 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
                 R.det |= u8_chunk_end_check(R);
             u8u16_round<2, Boundary, BE>(R, r, base, tile_off, chunk, lane_off, lo_b, hi_b, sbase, sel, running, err,
                                          err_pos, units);
+            if (err) // only a general round can find an error
+                break;
         }
-        if (err)
-            break;
     }
     if (!err)
         units = running;
