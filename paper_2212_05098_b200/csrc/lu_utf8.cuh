@@ -637,6 +637,47 @@ __device__ __forceinline__ void u8u16_round(const U8Round &R, int r, const uint8
 
 // BE: emit UTF-16BE (the word's high byte first): the compaction prmt takes
 // its two byte planes in the other order, at no cost.
+// Straight-line chunk for an interior warp whose prediction is the fast
+// class P: all four rounds take P's detector and tail with no branch between
+// them (each round's prediction vote is only OR-ed into the result), so the
+// compiler can overlap the rounds.  Returns nonzero if some round left the
+// class (or lane 31's chunk-end check fired): the caller then redoes the chunk
+// with the adaptive per-round path, which overwrites the staging region.
+template <int P, bool BE>
+__device__ __forceinline__ uint32_t u8u16_chunk_fast(const uint8_t *__restrict__ base, int64_t tile_off,
+                                                     int64_t chunk, int64_t lo_b, int64_t hi_b, uint32_t sbase,
+                                                     const SelPair *sel, const ChunkIn &in, const uint32_t *rn,
+                                                     uint32_t &running)
+{
+    const uint32_t lane = lane_id();
+    constexpr int kRounds = kChunkBytes / 512;
+    const uint4 *q = in.q;
+    uint32_t carry = in.halo_p;
+    uint32_t miss = 0, err = 0, err_pos = 0, units = 0;
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+        const int64_t lane_off = chunk + r * 512 + 16 * (int64_t)lane;
+        const uint32_t rp = __shfl_sync(0xffffffffu, q[r].w, (lane + 31) & 31);
+        U8Round R;
+        R.w[0] = (lane == 0) ? carry : rp;
+        carry = rp;
+        R.w[1] = q[r].x;
+        R.w[2] = q[r].y;
+        R.w[3] = q[r].z;
+        R.w[4] = q[r].w;
+        R.w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : in.halo_n) : rn[r];
+        uint32_t fd = P == 0 ? u8_fast0(R) : P == 1 ? u8_fast1(R) : u8_fast3(R);
+        if (r == kRounds - 1 && lane == 31)
+            fd |= u8_chunk_end_check(R);
+        miss |= __any_sync(0xffffffffu, fd != 0) ? 1u : 0u;
+        R.path = P;
+        R.det = 0;
+        u8u16_round<P, false, BE>(R, r, base, tile_off, chunk, lane_off, lo_b, hi_b, sbase, sel, running, err,
+                                  err_pos, units);
+    }
+    return miss;
+}
+
 template <bool Boundary, bool BE = false>
 __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int64_t tile_off, int64_t lo_b,
                                            int64_t hi_b, uint16_t *out_w, const SelPair *sel, WarpResult &wr,
@@ -656,6 +697,25 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
 
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(out_w);
     uint32_t running = 0, err = 0, err_pos = 0, units = 0;
+
+    if (!Boundary && hint != 2) {
+        uint32_t miss;
+        if (hint == 0)
+            miss = u8u16_chunk_fast<0, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
+        else if (hint == 1)
+            miss = u8u16_chunk_fast<1, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
+        else
+            miss = u8u16_chunk_fast<3, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
+        if (!miss) {
+            if (lane == 0) {
+                wr.err = 0;
+                wr.pos = 0;
+                wr.units = running;
+            }
+            return;
+        }
+        running = 0; // redo the chunk round by round
+    }
 
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
