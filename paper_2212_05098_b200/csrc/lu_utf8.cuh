@@ -698,14 +698,12 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(out_w);
     uint32_t running = 0, err = 0, err_pos = 0, units = 0;
 
-    if (!Boundary && hint != 2) {
+    if (!Boundary && hint < 2) {
         uint32_t miss;
         if (hint == 0)
             miss = u8u16_chunk_fast<0, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
-        else if (hint == 1)
-            miss = u8u16_chunk_fast<1, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
         else
-            miss = u8u16_chunk_fast<3, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
+            miss = u8u16_chunk_fast<1, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
         if (!miss) {
             if (lane == 0) {
                 wr.err = 0;
