@@ -95,7 +95,7 @@ def launch_shares(path):
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "")
         us = v / 1e3 if unit in ("nsecond", "ns") else v * (1e3 if unit in ("msecond", "ms") else 1)
-        if "lu::" not in r["Kernel Name"]:
+        if not any(t in r["Kernel Name"] for t in ("lu::", "k_transcode", "k_validate")):
             continue  # torch kernels of the seeded input generator (set-up, outside the step)
         k = short(r["Kernel Name"])
         tot[k] += us
