@@ -175,7 +175,12 @@ constexpr int kScanWarps = 8;
 #define LU_SCAN_PER_LANE 4
 #endif
 constexpr int kScanPerLane = LU_SCAN_PER_LANE;
-constexpr uint32_t kScanWindow = 32 * kScanPerLane; // 128 tiles
+constexpr uint32_t kScanWindow = 32 * kScanPerLane; // 128 tiles (K1)
+// K2 scans 256-tile windows: its tiles complete faster on latin / cyrillic,
+// where the per-window hand-off is the limit
+#ifndef LU_K2_SCAN_PER_LANE
+#define LU_K2_SCAN_PER_LANE 8
+#endif
 #ifndef LU_PARTIAL_AFTER
 #define LU_PARTIAL_AFTER 40000
 #endif
@@ -195,18 +200,20 @@ __device__ __forceinline__ void scan_init(ScanShared &ss)
         ss.errw = 0xffffffffu;
 }
 
+template <int kPL = kScanPerLane>
 __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, uint32_t sw, ScanShared &ss)
 {
+    constexpr uint32_t kWin = 32 * kPL; // tiles per window
     const uint32_t lane = lane_id();
-    const uint32_t nwin = (ntiles + kScanWindow - 1) / kScanWindow;
+    const uint32_t nwin = (ntiles + kWin - 1) / kWin;
     volatile unsigned long long *vbase = ss.base;
     volatile uint32_t *vtag = ss.tag;
     volatile uint32_t *verrw = &ss.errw;
     for (uint32_t w = sw; w < nwin; w += kScanWarps) {
-        const uint32_t t0 = w * kScanWindow + lane * kScanPerLane;
+        const uint32_t t0 = w * kWin + lane * kPL;
         unsigned long long base = 0;
         bool have_base = w == 0; // the base is taken only when first needed
-        uint64_t s[kScanPerLane];
+        uint64_t s[kPL];
         uint32_t have = 0; // bit j: s[j] holds a published aggregate
         uint32_t done = 0; // entries of the window already replaced by prefixes
         long long t_first = 0; // clock when the first tile of the window was seen
@@ -232,8 +239,8 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
             }
             if (have_base && (base & kErrBit)) {
 #pragma unroll
-                for (int j = 0; j < kScanPerLane; ++j)
-                    if (lane * kScanPerLane + j >= done && t0 + j < ntiles)
+                for (int j = 0; j < kPL; ++j)
+                    if (lane * kPL + j >= done && t0 + j < ntiles)
                         st_release(&status[t0 + j], kFlagInc | kErrBit | (base & kValMask));
                 if (lane == 0) {
                     atomicMin(&ss.errw, w);
@@ -244,7 +251,7 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                 break;
             }
 #pragma unroll
-            for (int j = 0; j < kScanPerLane; ++j)
+            for (int j = 0; j < kPL; ++j)
                 if (!(have & (1u << j))) {
                     const uint32_t t = t0 + j;
                     s[j] = t < ntiles ? ld_acquire(&status[t]) : kFlagAgg;
@@ -253,12 +260,12 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                 }
             // leading published run of the window: lanes before the first
             // lane with a gap are full; that lane contributes its own run
-            const uint32_t lrun = (uint32_t)__ffs(~have) - 1; // 0..kScanPerLane
-            const uint32_t notfull = __ballot_sync(0xffffffffu, lrun < kScanPerLane);
+            const uint32_t lrun = (uint32_t)__ffs(~have) - 1; // 0..kPL
+            const uint32_t notfull = __ballot_sync(0xffffffffu, lrun < kPL);
             const uint32_t fl = notfull ? (uint32_t)__ffs(notfull) - 1 : 32u;
-            const uint32_t myr = lane < fl ? kScanPerLane : (lane == fl ? lrun : 0u);
-            const uint32_t run = kScanPerLane * fl + (fl < 32 ? __shfl_sync(0xffffffffu, lrun, fl & 31) : 0u);
-            if (!partial && run != kScanWindow) {
+            const uint32_t myr = lane < fl ? kPL : (lane == fl ? lrun : 0u);
+            const uint32_t run = kPL * fl + (fl < 32 ? __shfl_sync(0xffffffffu, lrun, fl & 31) : 0u);
+            if (!partial && run != kWin) {
                 if (__any_sync(0xffffffffu, have != 0)) {
                     const long long now = clock64();
                     if (t_first == 0)
@@ -267,7 +274,7 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                 }
                 partial = __shfl_sync(0xffffffffu, partial, 0);
             }
-            if (run > done && (partial || run == kScanWindow)) {
+            if (run > done && (partial || run == kWin)) {
                 LU_CNT(11, 1);
                 if (!have_base) {
                     // Wait for the previous window's base, or for a window
@@ -294,9 +301,9 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                     base = ready == 1 ? vbase[slot] : kErrBit;
                     have_base = true;
                 }
-                uint32_t lsum = 0, errj = kScanPerLane;
+                uint32_t lsum = 0, errj = kPL;
 #pragma unroll
-                for (int j = kScanPerLane - 1; j >= 0; --j)
+                for (int j = kPL - 1; j >= 0; --j)
                     if ((uint32_t)j < myr) {
                         lsum += (uint32_t)s[j]; // aggregate counts are < 2^15
                         if (s[j] & kErrBit)
@@ -309,23 +316,23 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                     if (lane >= (uint32_t)d)
                         incl += o;
                 }
-                const uint32_t errball = __ballot_sync(0xffffffffu, errj < kScanPerLane);
+                const uint32_t errball = __ballot_sync(0xffffffffu, errj < kPL);
                 const bool err_before = (base & kErrBit) || (errball & ((1u << lane) - 1u));
                 uint64_t ex = (base & kValMask) + (incl - lsum);
 #pragma unroll
-                for (int j = 0; j < kScanPerLane; ++j) {
-                    const uint32_t idx = lane * kScanPerLane + j;
+                for (int j = 0; j < kPL; ++j) {
+                    const uint32_t idx = lane * kPL + j;
                     if ((uint32_t)j < myr && idx >= done && t0 + j < ntiles)
                         st_release(&status[t0 + j],
                                    kFlagInc | ((err_before || errj < (uint32_t)j) ? kErrBit : 0ull) | ex);
                     ex += (uint32_t)s[j];
                 }
                 done = run;
-                if (errball && run < kScanWindow) {
+                if (errball && run < kWin) {
                     // the rest of the window lies behind an error: publish it now
 #pragma unroll
-                    for (int j = 0; j < kScanPerLane; ++j)
-                        if (lane * kScanPerLane + j >= run && t0 + j < ntiles)
+                    for (int j = 0; j < kPL; ++j)
+                        if (lane * kPL + j >= run && t0 + j < ntiles)
                             st_release(&status[t0 + j], kFlagInc | kErrBit | (base & kValMask));
                     if (lane == 0) {
                         atomicMin(&ss.errw, w);
@@ -335,7 +342,7 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                     }
                     break;
                 }
-                if (run == kScanWindow) {
+                if (run == kWin) {
                     const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
                     if (lane == 0) {
                         if (errball || (base & kErrBit))

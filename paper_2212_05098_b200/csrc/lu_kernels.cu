@@ -251,6 +251,7 @@ struct DirU8U16T {
     static constexpr int kStride = kOutStrideU16;
     static constexpr int kBufs = kBufsK1;
     static constexpr int kUnitShift = 0; // input positions are bytes
+    static constexpr int kScanPerLane = LU_SCAN_PER_LANE; // 128-tile scanner windows
     using In = ChunkIn;
     template <bool B>
     __device__ static void load(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, uint32_t wit,
@@ -276,6 +277,7 @@ struct DirU16U8T {
     static constexpr int kStride = kOutStrideU8;
     static constexpr int kBufs = kBufsK2;
     static constexpr int kUnitShift = 1; // input positions are 16-bit words
+    static constexpr int kScanPerLane = LU_K2_SCAN_PER_LANE; // 256-tile windows
     using In = ChunkIn;
     template <bool B>
     __device__ static void load(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, uint32_t wit,
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     const uint32_t warp = threadIdx.x >> 5;
     LU_PROF_INIT();
     if (blockIdx.x == 0) {
-        scan_windows(status, ntiles, warp, scan_s);
+        scan_windows<Dir::kScanPerLane>(status, ntiles, warp, scan_s);
         LU_PROF_FLUSH();
         return;
     }
