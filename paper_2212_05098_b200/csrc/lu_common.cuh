@@ -176,10 +176,10 @@ constexpr int kScanWarps = 8;
 #endif
 constexpr int kScanPerLane = LU_SCAN_PER_LANE;
 constexpr uint32_t kScanWindow = 32 * kScanPerLane; // 128 tiles (K1)
-// K2 scans 256-tile windows: its tiles complete faster on latin / cyrillic,
+// K2 scans 192-tile windows: its tiles complete faster on latin / cyrillic,
 // where the per-window hand-off is the limit
 #ifndef LU_K2_SCAN_PER_LANE
-#define LU_K2_SCAN_PER_LANE 8
+#define LU_K2_SCAN_PER_LANE 6
 #endif
 #ifndef LU_PARTIAL_AFTER
 #define LU_PARTIAL_AFTER 40000

@@ -277,7 +277,7 @@ struct DirU16U8T {
     static constexpr int kStride = kOutStrideU8;
     static constexpr int kBufs = kBufsK2;
     static constexpr int kUnitShift = 1; // input positions are 16-bit words
-    static constexpr int kScanPerLane = LU_K2_SCAN_PER_LANE; // 256-tile windows
+    static constexpr int kScanPerLane = LU_K2_SCAN_PER_LANE; // 192-tile windows
     using In = ChunkIn;
     template <bool B>
     __device__ static void load(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, uint32_t wit,
