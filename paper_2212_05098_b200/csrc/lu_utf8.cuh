@@ -27,6 +27,8 @@
 
 #include "lu_common.cuh"
 
+#include <type_traits>
+
 namespace lu {
 
 struct U8Masks {
@@ -791,10 +793,12 @@ __device__ __forceinline__ void u8val_warp_in(const uint8_t *__restrict__ base, 
     for (int r = 0; r < kRounds; ++r)
         rn[r] = __shfl_sync(0xffffffffu, q[r].x, (lane + 1) & 31);
     uint32_t err = 0, err_pos = 0;
-    // straight-line chunk when the prediction is path 0 or 1 (as K1's
+    // straight-line chunk when the prediction is path 0, 1 or 3 (as K1's
     // u8u16_chunk_fast): four detector rounds, votes OR-ed, no branches
-    // between them; redo round by round if a round left the class
-    if (!Boundary && hint < 2) {
+    // between them; redo round by round if a round left the class.  Path 3
+    // has its own copy so the path 0 / 1 code stays as it was.
+    auto chunk_fast = [&](auto pc) -> bool {
+        constexpr int P = decltype(pc)::value;
         uint32_t miss = 0, cf = 0, cy = in.halo_p;
 #pragma unroll
         for (int r = 0; r < kRounds; ++r) {
@@ -807,26 +811,34 @@ __device__ __forceinline__ void u8val_warp_in(const uint8_t *__restrict__ base, 
             R.w[3] = q[r].z;
             R.w[4] = q[r].w;
             R.w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : halo_n) : rn[r];
-            uint32_t fd = hint == 0 ? u8_fast0(R) : u8_fast1(R);
+            uint32_t fd = P == 3 ? u8_fast3(R) : (hint == 0 ? u8_fast0(R) : u8_fast1(R));
             if (r == kRounds - 1 && lane == 31)
                 fd |= u8_chunk_end_check(R);
             miss |= __any_sync(0xffffffffu, fd != 0) ? 1u : 0u;
             if (Count) {
 #pragma unroll
                 for (int k = 1; k <= 4; ++k)
-                    cf += (~R.m[k].C & H8) >> 7; // no F bytes in paths 0 / 1
+                    cf += P == 3 ? ((~R.m[k].C & H8) >> 7) + (R.m[k].F >> 7)
+                                 : (~R.m[k].C & H8) >> 7; // no F bytes in paths 0 / 1
             }
         }
-        if (!miss) {
-            if (lane == 0) {
-                wr.err = 0;
-                wr.pos = 0;
-                wr.units = 0;
-            }
-            if (Count)
-                *count = (cf * 0x01010101u) >> 24;
+        if (miss)
+            return false;
+        if (lane == 0) {
+            wr.err = 0;
+            wr.pos = 0;
+            wr.units = 0;
+        }
+        if (Count)
+            *count = (cf * 0x01010101u) >> 24;
+        return true;
+    };
+    if (!Boundary && hint < 2) {
+        if (chunk_fast(std::integral_constant<int, 0>{}))
             return;
-        }
+    } else if (!Boundary && !Count && hint == 3) {
+        if (chunk_fast(std::integral_constant<int, 3>{}))
+            return;
     }
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
