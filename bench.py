@@ -13,10 +13,15 @@ buffers (H2D of the input, D2H of the outcome and of the written payload
 inside the timed region).  Extra keys carry config 3 (UTF-16LE -> UTF-8) and
 config 4 (validate) numbers measured in the same run.
 
-Multi-GPU (torchrun, one rank per GPU): every rank transcodes its own four
-buffers (weak scaling) and the per-shard outcomes are exchanged each step
-with one NCCL all_gather of int64[3] per buffer -- the only data-path
-collective of the sharded design.
+Multi-GPU (one process per GPU; ``--gpus N`` relaunches itself under
+``torch.distributed.run`` when it is not already running under it): the
+headline is weak scaling -- every rank transcodes its own four config-2
+buffers and the per-buffer outcomes are exchanged each step with one NCCL
+all_gather.  ``extras.config5_sharded`` is north_star's config 5: one 16 GiB
+input per direction cut at character boundaries across the N ranks
+(shard.snap_cut), each rank transcoding its shard in its own HBM and one
+NCCL all_gather of the per-shard (status, consumed, written, begin) records
+inside the timed step (shard.transcode_sharded); aggregate GiB/s at N.
 
 ``--impl reference`` times the reference algorithm's CPU restatement
 (oracle/, C, all host threads, character-boundary sharded) on the same
@@ -47,6 +52,20 @@ METRIC = "input GiB/s transcoded+validated (device-timed) and % of HBM roofline"
 GIB = float(1 << 30)
 EV_EVERY = 8  # steps of the timed region that carry per-launch timing events
 REF_BUDGET_S = 150.0  # --impl reference: bound on the timed CPU run
+WORKLOAD = ("config2: UTF-8->UTF-16LE, 4 x 256 MiB valid buffers per GPU "
+            "(latin/cyrillic/cjk/emoji, seeds 1-4 (+100*rank))")
+DATA = "synthetic (seeded SplitMix64 profiles, paper_2212_05098_b200/corpus.py)"
+C5_BYTES = 16 << 30  # config 5: 16 GiB per direction
+
+
+def bench_config(world: int) -> dict:
+    """The ``config`` object of both arms (identical, so the driver can pair them)."""
+    return {
+        "workload": WORKLOAD,
+        "input_bytes_per_step": world * len(PROFILES) * BUF_BYTES,
+        "l2": "inputs larger than L2 (256 MiB each > 126 MB), no flush",
+        "parallelism": f"dp{world} (independent shards, NCCL all_gather of outcomes)" if world > 1 else "dp1",
+    }
 
 
 def measured_peak():
@@ -186,11 +205,8 @@ def run_reference(args):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u8",
-        "data": "synthetic (seeded SplitMix64 profiles, corpus.py)",
-        "config": {
-            "workload": "config2: UTF-8->UTF-16LE, 4 x 256 MiB profiles (latin/cyrillic/cjk/emoji, seeds 1-4)",
-            "input_bytes_per_step": step_bytes,
-        },
+        "data": DATA,
+        "config": bench_config(world),
         "cpu_baseline": {
             "value": round(value, 3),
             "unit": "GiB/s",
@@ -208,7 +224,10 @@ def run_reference(args):
 
 
 def cpu_baseline_sample():
-    """Oracle on a bounded sample of the same workload (rank 0, N=1)."""
+    """Oracle on a bounded sample of the same workload (rank 0, N=1), plus
+    bounded CPU figures for configs 1, 3 and 4 and the reference's own Python
+    implementation when it is installed in
+    baseline/_ref."""
     import oracle
 
     from paper_2212_05098_b200 import corpus
@@ -224,7 +243,7 @@ def cpu_baseline_sample():
     t0 = time.perf_counter()
     oracle.run_mt(oracle.OP_U8_U16, bufs[2][: 16 << 20], 1, outs[2])
     dt_1 = time.perf_counter() - t0
-    return {
+    line = {
         "value": round(len(bufs) * sample / GIB / dt_mt, 3),
         "unit": "GiB/s",
         "cores": threads,
@@ -232,6 +251,188 @@ def cpu_baseline_sample():
         "sample": f"first 64 MiB of each config-2 profile buffer (256 MiB), oracle/laneutf_oracle.c "
         f"on {threads} host threads; single-thread cjk 16 MiB = {16 / 1024 / dt_1:.3f} GiB/s",
     }
+    # the other configs, same oracle, all host threads, bounded samples
+    per = {}
+
+    def timed(op, data, out=None, reps=1):
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            r = oracle.run_mt(op, data, threads, out)
+        return time.perf_counter() - t0, r
+
+    c1 = corpus.generate("mix", 4 << 20, 0, device="cuda").cpu().numpy()
+    w1 = np.empty(4 << 20, dtype=np.uint16)
+    t_a, r = timed(oracle.OP_U8_U16, c1, w1, reps=5)
+    words = w1[: r[2]].view(np.uint8)
+    t_b, _ = timed(oracle.OP_U16_U8, words, np.empty(3 * r[2], dtype=np.uint8), reps=5)
+    per["config1_round_trip_4MiB"] = {"gib_s": round(5 * (4 << 20) / GIB / (t_a + t_b), 3),
+                                      "sample": "4 MiB, both directions, 5 reps"}
+    c3 = {}
+    for (p, sd) in PROFILES:
+        w = corpus.generate(p, sample // 2, sd, utf16=True, device="cuda").cpu().numpy()
+        t, _ = timed(oracle.OP_U16_U8, w, np.empty(3 * (sample // 2), dtype=np.uint8))
+        c3[p] = round(sample / GIB / t, 3)
+    per["config3_utf16_to_utf8"] = {"gib_s": c3, "sample": "64 MiB (32 Mi words) per profile"}
+    e16 = corpus.generate("emoji", sample // 2, 4, utf16=True, device="cuda").cpu().numpy()
+    t_v8, _ = timed(oracle.OP_VAL_U8, bufs[2])
+    t_v16, _ = timed(oracle.OP_VAL_U16, e16)
+    per["config4_validate"] = {"cjk_utf8_gib_s": round(sample / GIB / t_v8, 3),
+                               "emoji_utf16_gib_s": round(sample / GIB / t_v16, 3),
+                               "sample": "64 MiB zero-error buffers"}
+    line["per_config"] = per
+    line["reference_python"] = reference_python_baseline(bufs, c1, threads)
+    return line
+
+
+def reference_python_baseline(bufs, c1, threads: int) -> dict:
+    """The reference package itself (pure Python, baseline/_ref) timed on the
+    host: (i) ``laneutf.bench.run_bench`` with the
+    scalar engine, one pinned core, on a 1 MiB character-aligned sample of each
+    config-2 profile; (ii) the same engine over all cores as one worker process
+    per core on 1 MiB character-aligned pieces; (iii) ``emulated-64`` (the
+    paper's algorithm in Python) on a 16 KiB sample of config 1."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "laneutf")):
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref the reference)"}
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    try:
+        from laneutf import bench as lbench
+    except Exception as exc:  # pragma: no cover
+        return {"unavailable": repr(exc)[:200]}
+
+    def aligned(b: np.ndarray, k: int) -> bytes:
+        while k < len(b) and (int(b[k]) & 0xC0) == 0x80:
+            k += 1
+        return b[:k].tobytes()
+
+    out = {"kind": "reference (laneutf 0.1.0, pure Python, baseline/_ref)"}
+    single = {}
+    for (p, _), b in zip(PROFILES, bufs):
+        rep, _payload = lbench.run_bench("utf8-to-utf16", aligned(b, 1 << 20), engine="scalar", repetitions=1,
+                                         warmup=0, label=p)
+        single[p] = round(rep.bytes_per_second / 2**20, 3)
+    out["scalar_1core_mib_s"] = single
+    # all cores: one process per core, each a 1 MiB character-aligned piece
+    import multiprocessing as mp
+
+    pieces = []
+    for b in bufs:
+        pos = 0
+        for _ in range(max(1, threads // len(bufs))):
+            end = pos + (1 << 20)
+            while end < len(b) and (int(b[end]) & 0xC0) == 0x80:
+                end += 1
+            pieces.append(b[pos:end].tobytes())
+            pos = end
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(threads, initializer=_ref_worker_init, initargs=(ref_dir,)) as pool:
+        pool.map(_ref_worker, pieces[:threads])  # warm the workers (imports)
+        t0 = time.perf_counter()
+        total = sum(pool.map(_ref_worker, pieces))
+        dt = time.perf_counter() - t0
+    out["scalar_all_cores"] = {"mib_s": round(total / 2**20 / dt, 3), "cores": threads,
+                               "sample": f"{len(pieces)} pieces of 1 MiB from the 4 profiles, one process per core"}
+    rep, _payload = lbench.run_bench("utf8-to-utf16", aligned(c1, 16 << 10), engine="emulated-64", repetitions=1,
+                                     warmup=0, label="config1")
+    out["emulated64_config1_mib_s"] = round(rep.bytes_per_second / 2**20, 4)
+    return out
+
+
+def _ref_worker_init(ref_dir: str) -> None:
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+
+
+def _ref_worker(piece: bytes) -> int:
+    from laneutf import engine as lengine
+
+    outcome, _payload = lengine.transcode_to_bytes("utf8-to-utf16", piece, engine="scalar")
+    assert outcome.status.value == "ok"
+    return len(piece)
+
+
+def config5_sharded(utf16: bool, world: int, rank: int, dev: torch.device, peak: float, steps: int = 3) -> dict:
+    """North_star config 5 on ``world`` GPUs: 16 GiB (UTF-8 bytes, or 8 Gi
+    UTF-16 words) of seeded 64 MiB profile segments, cut at character
+    boundaries (shard.snap_cut on the units at each nominal cut r*n/world).
+    Each rank generates only its shard plus 4 units of look-ahead, transcodes
+    it in its own HBM, and the timed step ends with shard.transcode_sharded:
+    one NCCL all_gather of (status, consumed, written, begin) per rank and the
+    global combine.  Returns the aggregate input GiB/s (max-over-ranks device
+    time) and the combined outcome."""
+    import torch.distributed as dist
+
+    from paper_2212_05098_b200 import UTF8_TO_UTF16, UTF16_TO_UTF8, corpus, outcome_from_tensor, transcode_device
+    from paper_2212_05098_b200.shard import combine_records, snap_cut, transcode_sharded
+
+    unit = 2 if utf16 else 1
+    n = C5_BYTES // unit
+    x0, x1 = n * rank // world, n * (rank + 1) // world
+    log(f"config 5 {'utf16->utf8' if utf16 else 'utf8->utf16'}: rank {rank} units [{x0}, {x1})")
+    win = corpus.config5_range(n, x0, min(x1 + 4, n), utf16=utf16, device=dev)
+    wv = win.view(torch.int16) if utf16 else win
+
+    def units_at(pos: int) -> list[int]:
+        return [v & 0xFFFF for v in wv[pos - x0: pos - x0 + 4].cpu().tolist()]
+
+    def snap(x: int) -> int:
+        if x <= 0 or x >= n:
+            return max(0, min(x, n))
+        head = units_at(x)
+        return snap_cut(lambda i: head[i - x] if i - x < len(head) else 0, n, x, utf16)
+
+    begin, end = snap(x0), snap(x1)
+    shard = win[unit * (begin - x0): unit * (end - x0)]
+    direction = UTF16_TO_UTF8 if utf16 else UTF8_TO_UTF16
+    stream = torch.cuda.current_stream(dev)
+    res, out = transcode_device(direction, shard)
+    if world > 1:
+        bounds = torch.tensor([begin, end], dtype=torch.int64, device=dev)
+        allb = [torch.empty_like(bounds) for _ in range(world)]
+        dist.all_gather(allb, bounds)
+        allb = [t.tolist() for t in allb]
+        assert all(allb[r][1] == allb[r + 1][0] for r in range(world - 1)), allb
+
+    def combine():
+        if world > 1:
+            return transcode_sharded(res, begin)
+        rec = [int(v) for v in res.cpu().tolist()]
+        st, consumed, written, _ = combine_records([(rec[0] & 0xFFFFFFFF, rec[1], rec[2])], [begin])
+        from paper_2212_05098_b200.outcome import STATUS_BY_CODE, TranscodeOutcome
+        return TranscodeOutcome(STATUS_BY_CODE[st], consumed, written)
+
+    got = combine()
+    outcome = got.outcome if world > 1 else got
+    local = outcome_from_tensor(res.cpu())
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        transcode_device(direction, shard, out, res=res)
+        combine()  # the all_gather (NCCL) and the global combine, inside the timed step
+    b.record(stream)
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / 1e3 / steps
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+        dist.barrier()
+    ab = C5_BYTES + (1 if utf16 else 2) * outcome.written
+    result = {"aggregate_input_gib_s": round(C5_BYTES / GIB / t, 2), "ms_per_step": round(t * 1e3, 3),
+              "n_gpus": world, "frac_of_measured_x_gpus": round(ab / t / 1e9 / (peak * world), 4),
+              "status": outcome.status.value, "consumed": outcome.consumed, "written": outcome.written,
+              "ok": outcome.ok and outcome.consumed == n,
+              "rank0_shard_units": end - begin, "rank0_local_written": local.written,
+              "collective": "NCCL all_gather of 4 x int64 per rank (shard.transcode_sharded)" if world > 1
+              else "none (1 rank: shard.combine_records only)",
+              "steps": steps}
+    del win, shard, out, res
+    torch.cuda.empty_cache()
+    return result
 
 
 def log(msg: str) -> None:
@@ -250,6 +451,21 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip config 3/4 side measurements")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch this command under torch.distributed.run
+        import socket
+        import subprocess
+
+        with socket.socket() as sock:
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if world_env != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world_env}: launch one process per GPU")
 
     if args.impl == "reference":
         run_reference(args)
@@ -375,15 +591,8 @@ def main():
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u8",
-        "data": "synthetic (seeded SplitMix64 profiles generated in HBM, corpus.py)",
-        "config": {
-            "workload": "config2: UTF-8->UTF-16LE, 4 x 256 MiB valid buffers per GPU "
-            "(latin/cyrillic/cjk/emoji, seeds 1-4 (+100*rank))",
-            "input_bytes_per_step": in_bytes,
-            "output_bytes_per_step": out_bytes,
-            "l2": "inputs larger than L2 (256 MiB each > 126 MB), no flush",
-            "parallelism": f"dp{world} (independent shards, NCCL all_gather of outcomes)" if world > 1 else "dp1",
-        },
+        "data": DATA,
+        "config": bench_config(world),
         "roofline": {
             "bound": "hbm",
             "achieved": round(achieved, 1),
@@ -394,6 +603,7 @@ def main():
             "kernel": "k_transcode<DirU8U16> (K1)",
             "algorithmic_bytes": "input bytes + 2 x written words, per launch",
             "alg_bytes_per_launch": round(float(alg_bytes.mean())),
+            "output_bytes_per_step": out_bytes,
             "traffic_source": "profiles/ncu_summary.json (ncu --set full, dram__bytes_read+write per launch)",
             "peak_source": peak_src,
             "per_profile": prof_detail,
@@ -408,19 +618,41 @@ def main():
     # ---- e2e through the public facade with pinned host buffers
     hosts = [s.cpu().pin_memory() for s in srcs]
     host_outs = [torch.empty(2 * BUF_BYTES, dtype=torch.uint8).pin_memory() for _ in srcs]
-    for h, ho in zip(hosts, host_outs):
-        transcode(UTF8_TO_UTF16, h, ho, engine="native")
+    expect = [(o.status, o.consumed, o.written) for o in outcomes]
+
+    def e2e_check(got, tag):
+        got = [(o.status, o.consumed, o.written) for o in got]
+        assert got == expect, (tag, got, expect)
+
+    e2e_check([transcode(UTF8_TO_UTF16, h, ho, engine="native") for h, ho in zip(hosts, host_outs)], "warm-up")
+    for o, ho in zip(outs, host_outs[:1]):  # payload spot check: the whole latin output
+        assert torch.equal(ho[: 2 * outcomes[0].written].to(dev), o.view(torch.uint8)[: 2 * outcomes[0].written])
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        for h, ho in zip(hosts, host_outs):
-            o = transcode(UTF8_TO_UTF16, h, ho, engine="native")
+        got = [transcode(UTF8_TO_UTF16, h, ho, engine="native") for h, ho in zip(hosts, host_outs)]
     e2e_s = time.perf_counter() - t0
+    e2e_check(got, "timed")
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
+    # host copies alone: H2D of the step's inputs and
+    # D2H of its payloads, each timed with CUDA events, no kernel
+    a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a_ev.record(stream)
+    for h, s_ in zip(hosts, srcs):
+        s_.copy_(h, non_blocking=True)
+    b_ev.record(stream)
+    torch.cuda.synchronize()
+    h2d_s = a_ev.elapsed_time(b_ev) / 1e3
+    a_ev.record(stream)
+    for o, ho, oc in zip(outs, host_outs, outcomes):
+        ho[: 2 * oc.written].copy_(o.view(torch.uint8)[: 2 * oc.written], non_blocking=True)
+    b_ev.record(stream)
+    torch.cuda.synchronize()
+    d2h_s = a_ev.elapsed_time(b_ev) / 1e3
     line["e2e"] = {
         "value": round(world * args.e2e_steps * in_bytes / GIB / e2e_s, 3),
         "unit": "GiB/s",
@@ -428,8 +660,23 @@ def main():
         "d2h_bytes_per_step": out_bytes + 24 * len(srcs),
         "steps": args.e2e_steps,
         "api": "paper_2212_05098_b200.transcode(UTF8_TO_UTF16, pinned_in, pinned_out, engine='native')",
+        "outcomes_checked": True,
+        "h2d_alone": {"ms": round(h2d_s * 1e3, 3), "gib_s": round(in_bytes / GIB / h2d_s, 2)},
+        "d2h_alone": {"ms": round(d2h_s * 1e3, 3), "gib_s": round(out_bytes / GIB / d2h_s, 2)},
     }
-    del hosts, host_outs
+    # the reference callers' types: bytes in, bytearray out (cli.py:92, bench.py:100-106)
+    log("e2e bytes")
+    blobs = [h.numpy().tobytes() for h in hosts]
+    ba_outs = [bytearray(2 * BUF_BYTES) for _ in srcs]
+    e2e_check([transcode(UTF8_TO_UTF16, bb, ba, engine="native") for bb, ba in zip(blobs, ba_outs)], "bytes")
+    t0 = time.perf_counter()
+    got = [transcode(UTF8_TO_UTF16, bb, ba, engine="native") for bb, ba in zip(blobs, ba_outs)]
+    eb_s = time.perf_counter() - t0
+    e2e_check(got, "bytes timed")
+    line["e2e"]["bytes_api"] = {
+        "value": round(in_bytes / GIB / eb_s, 3), "unit": "GiB/s",
+        "api": "transcode(UTF8_TO_UTF16, bytes, bytearray): pinned staging ring, chunked H2D / kernel / D2H"}
+    del hosts, host_outs, blobs, ba_outs
 
     # ---- extras: config 3 (UTF-16 -> UTF-8) and config 4 (validate), same run
     if not args.no_extras:
@@ -577,29 +824,11 @@ def main():
             cb[name] = {"cases": 1 << 24, "ms": round(t * 1e3, 2), "cases_per_s": round((1 << 24) / t)}
         extras["row8f_batch"] = cb
         del tri, tri_data, tri_offs
-        # config 5 on one GPU: 16 GiB of mixed-profile 64 MiB segments each way
-        if world == 1:
-            c5 = {}
-            for name, utf16 in (("utf8_to_utf16_16GiB", False), ("utf16_to_utf8_16GiB", True)):
-                units = (16 << 30) // (2 if utf16 else 1)
-                log(f"extras: config 5 {name}")
-                big = corpus.config5_generate(units, utf16=utf16, device=dev)
-                direction = UTF16_TO_UTF8 if utf16 else UTF8_TO_UTF16
-                res, bout = transcode_device(direction, big)
-                o = outcome_from_tensor(res.cpu())
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                for _ in range(3):
-                    transcode_device(direction, big, bout, res=res)
-                b.record(stream)
-                torch.cuda.synchronize()
-                t = a.elapsed_time(b) / 1e3 / 3
-                ab = (16 << 30) + (1 if utf16 else 2) * o.written
-                c5[name] = {"input_gib_s": round(16 / t, 2), "frac_of_measured": round(ab / t / 1e9 / peak, 4),
-                            "ok": o.ok, "written": o.written}
-                del big, bout, res
-                torch.cuda.empty_cache()
-            extras["config5_single_gpu"] = c5
+        # config 5: 16 GiB per direction cut at character boundaries across the
+        # ranks; every rank transcodes its shard, one all_gather of records
+        extras["config5_sharded"] = {
+            name: config5_sharded(utf16, world, rank, dev, peak)
+            for name, utf16 in (("utf8_to_utf16_16GiB", False), ("utf16_to_utf8_16GiB", True))}
         line["extras"] = extras
 
     if rank == 0 and world == 1:

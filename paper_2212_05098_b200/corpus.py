@@ -350,3 +350,25 @@ def config5_generate(total_units: int, *, seed: int = 5, utf16: bool = False, de
         out[unit * pos: unit * (pos + units)] = generate(name, units, sseed, utf16=utf16, device=device)
         pos += units
     return out
+
+
+def config5_range(total_units: int, begin: int, end: int, *, seed: int = 5, utf16: bool = False, device="cuda",
+                  segment_units: int = 64 << 20) -> torch.Tensor:
+    """Units [begin, end) of the config-5 buffer (``config5_generate``)
+    without materialising the rest: only the segments overlapping the range
+    are generated.  Used by the multi-GPU driver, where each rank builds just
+    its shard (plus a few units of look-ahead for its end cut)."""
+    unit = 2 if utf16 else 1
+    begin, end = max(0, begin), min(end, total_units)
+    out = torch.empty(unit * max(end - begin, 0), dtype=torch.uint8, device=device)
+    pos = 0
+    for name, sseed, units in config5_segments(total_units, seed, segment_units, utf16):
+        lo, hi = max(pos, begin), min(pos + units, end)
+        if lo < hi:
+            seg = generate(name, units, sseed, utf16=utf16, device=device)
+            out[unit * (lo - begin): unit * (hi - begin)] = seg[unit * (lo - pos): unit * (hi - pos)]
+            del seg
+        pos += units
+        if pos >= end:
+            break
+    return out

@@ -77,6 +77,23 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v)
     return v;
 }
 
+// Hang guard: a spin-wait that sees no progress for kHangNs of GPU time
+// traps (a launch error the caller sees) instead of hanging the device.  No
+// valid schedule waits that long: every wait is on work of CTAs that are
+// already running (see k_transcode).
+constexpr uint64_t kHangNs = 10ull * 1000000000ull;
+__device__ __forceinline__ uint64_t gtimer()
+{
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void hang_check(uint32_t spins, uint64_t t0)
+{
+    if ((spins & 1023u) == 1023u && gtimer() - t0 > kHangNs)
+        __trap();
+}
+
 __device__ __forceinline__ uint32_t lane_id()
 {
     uint32_t l;
@@ -218,7 +235,9 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
         uint32_t done = 0; // entries of the window already replaced by prefixes
         long long t_first = 0; // clock when the first tile of the window was seen
         bool partial = false;
-        for (;;) {
+        const uint64_t t_win = gtimer();
+        for (uint32_t polls = 0;; ++polls) {
+            hang_check(polls, t_win);
             // Everything in a window behind an error is "error before": publish
             // it at once without waiting for the tiles (whose owners skip their
             // work, see k_transcode) -- groups then never wait on them.  (The
@@ -286,7 +305,9 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                     const uint32_t slot = (w - 1) % kScanWarps;
                     uint32_t ready = 0;
                     if (lane == 0) {
-                        for (;;) {
+                        const uint64_t t_wait = gtimer();
+                        for (uint32_t spins = 0;; ++spins) {
+                            hang_check(spins, t_wait);
                             if (vtag[slot] == w) {
                                 ready = 1;
                                 break;

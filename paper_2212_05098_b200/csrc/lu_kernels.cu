@@ -311,10 +311,12 @@ __device__ __forceinline__ void pipe_resolve(GroupShared &ps, uint32_t b, uint64
     if ((st >> kFlagShift) != 2)
         st = ld_acquire(&status[tile]);
     uint32_t spins = 0;
+    const uint64_t t0 = (st >> kFlagShift) != 2 ? gtimer() : 0;
     while ((st >> kFlagShift) != 2) {
         __nanosleep(32);
         st = ld_acquire(&status[tile]);
         ++spins;
+        hang_check(spins, t0);
     }
     LU_CNT(9, spins);
     LU_CNT(10, spins ? 1 : 0);
@@ -360,16 +362,27 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     __shared__ SelPair sel[40]; // K1 compaction selectors, then K2 path-C and path-A selectors
     __shared__ GroupShared gshared[kGroupsPerCta];
     __shared__ ScanShared scan_s;
+    __shared__ uint32_t role_s;
 
     const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n_bytes;
     unsigned int *ticket = reinterpret_cast<unsigned int *>(status + ntiles);
-    unsigned int *err_tile = ticket + 1; // zeroed with the status words
+    unsigned int *err_tile = ticket + 1;  // zeroed with the status words
+    unsigned int *role_ctr = ticket + 2;  // idem
     sel_table_init(sel);
     scan_init(scan_s);
+    // The scanner is the first CTA to start, not blockIdx 0: CUDA does not
+    // promise to dispatch blocks in index order, and other kernels (user
+    // streams, MPS, NCCL) may hold SMs, so a fixed scanner CTA could still be
+    // waiting for a slot while the workers that depend on it spin.  The
+    // first CTA to take a role ticket is running by construction; every
+    // other wait is on tiles claimed by running CTAs, so the kernel makes
+    // progress whatever subset of its CTAs is resident.
+    if (threadIdx.x == 0)
+        role_s = atomicAdd(role_ctr, 1u);
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5;
     LU_PROF_INIT();
-    if (blockIdx.x == 0) {
+    if (role_s == 0) {
         scan_windows<Dir::kScanPerLane>(status, ntiles, warp, scan_s);
         LU_PROF_FLUSH();
         return;
@@ -998,14 +1011,14 @@ static int u8u16_impl(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint64
         return fail(LU_ERR_INVALID, "null output");
     const uint32_t lead = (uint32_t)((uintptr_t)in & 15);
     const uint64_t nt = n_tiles(n_bytes, lead, kPipeTile);
-    if (ws_bytes < 8 * (nt + 1)) // tile status words + the tile ticket counter
+    if (ws_bytes < 8 * (nt + 2)) // tile status words + ticket / error-tile / role counters
         return fail(LU_ERR_WORKSPACE, "workspace too small (see lu_workspace_bytes)");
     if (nt > 0x7fffffffull)
         return fail(LU_ERR_INVALID, "input too large");
     int rc = set_smem_attrs();
     if (rc)
         return rc;
-    cudaError_t e = cudaMemsetAsync(ws, 0, 8 * (nt + 1), stream);
+    cudaError_t e = cudaMemsetAsync(ws, 0, 8 * (nt + 2), stream);
     if (e != cudaSuccess)
         return cuda_fail(e, "cudaMemsetAsync");
     const uint8_t *base = in ? in - lead : reinterpret_cast<const uint8_t *>(16);
@@ -1040,14 +1053,14 @@ static int u16u8_impl(const uint16_t *in, uint64_t n_words, uint8_t *out, uint64
     const uint8_t *inb = reinterpret_cast<const uint8_t *>(in);
     const uint32_t lead = (uint32_t)((uintptr_t)inb & 15);
     const uint64_t nt = n_tiles(2 * n_words, lead, kPipeTile);
-    if (ws_bytes < 8 * (nt + 1)) // tile status words + the tile ticket counter
+    if (ws_bytes < 8 * (nt + 2)) // tile status words + ticket / error-tile / role counters
         return fail(LU_ERR_WORKSPACE, "workspace too small (see lu_workspace_bytes)");
     if (nt > 0x7fffffffull)
         return fail(LU_ERR_INVALID, "input too large");
     int rc = set_smem_attrs();
     if (rc)
         return rc;
-    cudaError_t e = cudaMemsetAsync(ws, 0, 8 * (nt + 1), stream);
+    cudaError_t e = cudaMemsetAsync(ws, 0, 8 * (nt + 2), stream);
     if (e != cudaSuccess)
         return cuda_fail(e, "cudaMemsetAsync");
     const uint8_t *base = inb ? inb - lead : reinterpret_cast<const uint8_t *>(16);
@@ -1131,10 +1144,10 @@ uint64_t lu_workspace_bytes(int op, uint64_t n_units)
     switch (op) {
     case LU_OP_UTF8_TO_UTF16LE:
     case LU_OP_UTF8_TO_UTF16BE:
-        return 8 * (n_tiles(n_units, 15, kPipeTile) + 1) + 64;
+        return 8 * (n_tiles(n_units, 15, kPipeTile) + 2) + 64;
     case LU_OP_UTF16LE_TO_UTF8:
     case LU_OP_UTF16BE_TO_UTF8:
-        return 8 * (n_tiles(2 * n_units, 15, kPipeTile) + 1) + 64;
+        return 8 * (n_tiles(2 * n_units, 15, kPipeTile) + 2) + 64;
     case LU_OP_VALIDATE_UTF8:
     case LU_OP_VALIDATE_UTF16LE:
     case LU_OP_UTF16_LENGTH_FROM_UTF8:

@@ -36,7 +36,6 @@ import torch
 from . import _native, hostpipe
 from .outcome import STATUS_BY_CODE, TranscodeOutcome, TranscodeStatus
 
-_PIPELINE_MIN_BYTES = 8 << 20  # pinned host buffers at least this large use the chunked pipeline
 
 __all__ = [
     "UTF8_TO_UTF16",
@@ -121,11 +120,37 @@ def parse_engine(text: str) -> EngineKind:
     raise ValueError(f"cannot parse engine name {text!r}")
 
 
+def _parse_cpu_features(cpuinfo_text: str) -> frozenset[str]:
+    """``flags`` / ``Features`` lines of /proc/cpuinfo (engine.py:106-112)."""
+    features: set[str] = set()
+    for line in cpuinfo_text.splitlines():
+        key, _, value = line.partition(":")
+        if key.strip().lower() in ("flags", "features"):
+            features.update(value.split())
+    return frozenset(features)
+
+
+def _host_features() -> frozenset[str]:
+    try:
+        with open("/proc/cpuinfo", encoding="ascii", errors="replace") as fh:
+            return _parse_cpu_features(fh.read())
+    except OSError:
+        return frozenset()
+
+
 @dataclass(frozen=True)
 class EngineInventory:
+    """Same fields as the reference (engine.py:132-136) -- ``kinds``,
+    ``cpu_features``, ``native_capable_host`` -- plus the device name and,
+    when the native engine cannot run, the reason.  ``native_capable_host``
+    here means "this host can run the native engine" (a B200 is visible and
+    the library loads): the B200 engine's prerequisite is the GPU, not a CPU
+    feature set."""
+
     kinds: tuple[EngineKind, ...]
-    device_name: str | None
+    cpu_features: frozenset[str]
     native_capable_host: bool
+    device_name: str | None = None
     reason: str | None = None
 
     def available(self, kind: EngineKind) -> bool:
@@ -138,7 +163,8 @@ def detect() -> EngineInventory:
     reason = _native.unavailable_reason()
     name = torch.cuda.get_device_name() if torch.cuda.is_available() else None
     kinds = (EngineKind.native(),) if reason is None else ()
-    return EngineInventory(kinds=kinds, device_name=name, native_capable_host=reason is None, reason=reason)
+    return EngineInventory(kinds=kinds, cpu_features=_host_features(), native_capable_host=reason is None,
+                           device_name=name, reason=reason)
 
 
 def resolve_engine(engine: EngineKind | str | None = None) -> EngineKind:
@@ -228,6 +254,41 @@ def outcome_from_tensor(res: torch.Tensor) -> TranscodeOutcome:
     return TranscodeOutcome(status, int(v[1]), int(v[2]))
 
 
+def _side_stream(stream: torch.cuda.Stream | None, device: torch.device) -> torch.cuda.Stream | None:
+    """The stream to launch on, ordered after the current stream when it differs.
+
+    Inputs made contiguous, outputs, outcome records and workspaces allocated
+    here come from the caching allocator on the *current* stream; a launch on
+    another stream first waits for that stream (allocation and copies done),
+    and ``_keep_alive`` then ties those temporaries to the launch stream so
+    their blocks are not reused while the kernel still runs."""
+    if stream is None:
+        return None
+    cur = torch.cuda.current_stream(device)
+    if stream == cur:
+        return None
+    stream.wait_stream(cur)
+    return stream
+
+
+def _keep_alive(side: torch.cuda.Stream | None, *tensors: torch.Tensor | None) -> None:
+    if side is None:
+        return
+    for t in tensors:
+        if t is not None and t.is_cuda:
+            t.record_stream(side)
+
+
+def _check_out_tensor(out: torch.Tensor, device: torch.device) -> None:
+    """The kernels write ``numel * element_size`` contiguous bytes from
+    ``data_ptr``: a strided view or a tensor on another GPU would be
+    corrupted (or fault) silently."""
+    if not out.is_contiguous():
+        raise ValueError("output tensor must be contiguous")
+    if out.device != device:
+        raise ValueError(f"output tensor is on {out.device}, input on {device}")
+
+
 def transcode_device(
     direction: str,
     src: torch.Tensor,
@@ -244,13 +305,19 @@ def transcode_device(
     as uint8 of even length / int16 / uint16).  Returns ``(res, out)``:
     ``res`` is an int64[3] CUDA tensor with the lu_outcome (decode with
     ``outcome_from_tensor`` after the stream completes) and ``out`` the
-    worst-case output buffer (uint16 words or uint8 bytes).
+    worst-case output buffer (uint16 words or uint8 bytes).  With a
+    ``stream`` other than the current one, the launch is ordered after the
+    current stream's work and every temporary allocated here stays alive
+    until the launch stream is done with it.
     """
     _check_direction(direction)
     be = _check_byte_order(utf16_byte_order)
     device = src.device
+    if out is not None:
+        _check_out_tensor(out, device)
     srcb = _to_device_bytes(src, device)
     nbytes = srcb.numel()
+    own_out = out is None
     if direction == UTF8_TO_UTF16:
         op, n_units, cap = (_native.OP_UTF8_TO_UTF16BE if be else _native.OP_UTF8_TO_UTF16LE), nbytes, nbytes
         if out is None:
@@ -264,11 +331,15 @@ def transcode_device(
         if out is None:
             out = torch.empty(max(cap, 1), dtype=torch.uint8, device=device)
         out_cap = out.numel() * out.element_size()
+    own_res, own_ws = res is None, ws is None
     if res is None:
         res = torch.empty(3, dtype=torch.int64, device=device)
     if ws is None:
         ws = torch.empty(_native.workspace_bytes(op, n_units) // 8 + 1, dtype=torch.int64, device=device)
+    side = _side_stream(stream, device)
     _native.launch(op, srcb, n_units, out, out_cap, ws, res, stream)
+    _keep_alive(side, srcb if srcb.data_ptr() != src.data_ptr() else None, out if own_out else None,
+                res if own_res else None, ws if own_ws else None)
     return res, out
 
 
@@ -281,7 +352,8 @@ def validate_device(
     stream: torch.cuda.Stream | None = None,
     utf16_byte_order: str = "le",
 ) -> torch.Tensor:
-    """Device-resident validation; returns the int64[3] outcome tensor."""
+    """Device-resident validation; returns the int64[3] outcome tensor
+    (stream rules as ``transcode_device``)."""
     _check_direction(direction)
     be = _check_byte_order(utf16_byte_order)
     device = src.device
@@ -293,36 +365,23 @@ def validate_device(
         if nbytes % 2:
             raise ValueError("UTF-16 input must be an even number of bytes")
         op, n_units = (_native.OP_VALIDATE_UTF16BE if be else _native.OP_VALIDATE_UTF16LE), nbytes // 2
+    own_res, own_ws = res is None, ws is None
     if res is None:
         res = torch.empty(3, dtype=torch.int64, device=device)
     if ws is None:
         ws = torch.empty(_native.workspace_bytes(op, n_units) // 8 + 1, dtype=torch.int64, device=device)
+    side = _side_stream(stream, device)
     _native.launch(op, srcb, n_units, None, 0, ws, res, stream)
+    _keep_alive(side, srcb if srcb.data_ptr() != src.data_ptr() else None, res if own_res else None,
+                ws if own_ws else None)
     return res
 
 
 # ------------------------------------------------------------- facade
 
 
-def _write_payload(out, payload: torch.Tensor) -> None:
-    """Copy the written prefix (a CUDA uint8 tensor) into the caller's ``out``."""
-    k = payload.numel()
-    if isinstance(out, torch.Tensor):
-        dst = out.view(torch.uint8).reshape(-1) if out.dtype != torch.uint8 else out.reshape(-1)
-        if dst.numel() < k:
-            raise ValueError("output buffer smaller than the transcoded payload")
-        dst[:k].copy_(payload, non_blocking=dst.is_cuda or dst.is_pinned())
-        if not dst.is_cuda:
-            torch.cuda.current_stream().synchronize()
-        return
-    mv = memoryview(out).cast("B")
-    if mv.readonly:
-        raise ValueError("output buffer is read-only")
-    if mv.nbytes < k:
-        raise ValueError("output buffer smaller than the transcoded payload")
-    if k:
-        host = torch.frombuffer(mv, dtype=torch.uint8, count=k)
-        host.copy_(payload)
+def _is_device(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.is_cuda
 
 
 def transcode(
@@ -340,6 +399,12 @@ def transcode(
     prefix (``unit * written`` bytes); nothing past it is touched.
     ``utf16_byte_order="be"`` (keyword-only extension): the UTF-16 side is
     big-endian, byte swap fused into the kernels.
+
+    Host ``data`` and host ``out`` (``bytes`` / ``bytearray`` / memoryview /
+    numpy / CPU tensors, the reference callers' case) stream through a
+    reusable ring of chunk buffers with H2D, kernels and D2H overlapped
+    (hostpipe.py); pinned tensors are read and written in place.  A CUDA
+    ``data`` or ``out`` keeps the data on the device.
     """
     _check_direction(direction)
     be = _check_byte_order(utf16_byte_order)
@@ -347,34 +412,25 @@ def transcode(
     if direction == UTF16_TO_UTF8 and _byte_len(data) % 2:
         raise ValueError("UTF-16 input must be an even number of bytes")
     _require_native(kind)
-    if (
-        isinstance(data, torch.Tensor)
-        and isinstance(out, torch.Tensor)
-        and not data.is_cuda
-        and not out.is_cuda
-        and data.is_pinned()
-        and out.is_pinned()
-        and data.numel() * data.element_size() >= _PIPELINE_MIN_BYTES
-    ):
-        # pinned host in/out: chunked, overlapped H2D / kernel / D2H (hostpipe.py)
-        src = data.contiguous().view(torch.uint8).reshape(-1)
-        dst = out.view(torch.uint8).reshape(-1)
-        unit = 2 if direction == UTF8_TO_UTF16 else 1
-        cap = src.numel() if direction == UTF8_TO_UTF16 else 3 * (src.numel() // 2)
-        if dst.numel() < unit * cap:
-            raise ValueError("output buffer smaller than the worst case (worst_case_output_bytes)")
-        return hostpipe.pipelined_transcode(direction == UTF8_TO_UTF16, src, dst, be=be)
+    if not _is_device(data) and not _is_device(out):
+        if isinstance(out, torch.Tensor) and not out.is_contiguous():
+            raise ValueError("output tensor must be contiguous")
+        return hostpipe.stream_transcode(direction == UTF8_TO_UTF16, data, out, be=be)
     device = _device()
     src = _to_device_bytes(data, device)
-    out_dev = None
-    if isinstance(out, torch.Tensor) and out.is_cuda:
-        out_dev = out  # kernel writes straight into the caller's device buffer
+    out_dev = out if _is_device(out) else None
+    if out_dev is not None:
+        _check_out_tensor(out_dev, device)
     res, buf = transcode_device(direction, src, out_dev, utf16_byte_order=utf16_byte_order)
     outcome = outcome_from_tensor(res.cpu())
     if out_dev is None:
         unit = 2 if direction == UTF8_TO_UTF16 else 1
-        payload = buf.view(torch.uint8)[: unit * outcome.written]
-        _write_payload(out, payload)
+        sink = hostpipe.host_u8(out, writable=True)
+        k = unit * outcome.written
+        if sink.size < k:
+            raise ValueError("output buffer smaller than the transcoded payload")
+        if k:
+            hostpipe._t(sink[:k]).copy_(buf.view(torch.uint8)[:k])
     return outcome
 
 
@@ -387,16 +443,18 @@ def transcode_to_bytes(
 ) -> tuple[TranscodeOutcome, bytes]:
     """Transcode into a fresh worst-case buffer; returns outcome + payload (engine.py:212-223)."""
     _check_direction(direction)
-    _check_byte_order(utf16_byte_order)
+    be = _check_byte_order(utf16_byte_order)
     kind = resolve_engine(engine)
     if direction == UTF16_TO_UTF8 and _byte_len(data) % 2:
         raise ValueError("UTF-16 input must be an even number of bytes")
     _require_native(kind)
-    device = _device()
-    src = _to_device_bytes(data, device)
-    res, buf = transcode_device(direction, src, utf16_byte_order=utf16_byte_order)
-    outcome = outcome_from_tensor(res.cpu())
     unit = 2 if direction == UTF8_TO_UTF16 else 1
+    if not _is_device(data):
+        sink = np.empty(max(worst_case_output_bytes(direction, _byte_len(data)), 1), dtype=np.uint8)
+        outcome = hostpipe.stream_transcode(direction == UTF8_TO_UTF16, data, sink, be=be)
+        return outcome, sink[: unit * outcome.written].tobytes()
+    res, buf = transcode_device(direction, data, utf16_byte_order=utf16_byte_order)
+    outcome = outcome_from_tensor(res.cpu())
     payload = buf.view(torch.uint8)[: unit * outcome.written].cpu().numpy().tobytes()
     return outcome, payload
 
@@ -408,16 +466,17 @@ def validate(
     engine: EngineKind | str | None = None,
     utf16_byte_order: str = "le",
 ) -> TranscodeOutcome:
-    """Validation via the B200 read-only kernels; written is always 0 (engine.py:226-240)."""
+    """Validation via the B200 read-only kernels; written is always 0 (engine.py:226-240).
+    Host data streams through the chunk ring (hostpipe.stream_validate)."""
     _check_direction(direction)
-    _check_byte_order(utf16_byte_order)
+    be = _check_byte_order(utf16_byte_order)
     kind = resolve_engine(engine)
     if direction == UTF16_TO_UTF8 and _byte_len(data) % 2:
         raise ValueError("UTF-16 input must be an even number of bytes")
     _require_native(kind)
-    device = _device()
-    src = _to_device_bytes(data, device)
-    res = validate_device(direction, src, utf16_byte_order=utf16_byte_order)
+    if not _is_device(data):
+        return hostpipe.stream_validate(direction == UTF8_TO_UTF16, data, be=be)
+    res = validate_device(direction, data, utf16_byte_order=utf16_byte_order)
     outcome = outcome_from_tensor(res.cpu())
     return TranscodeOutcome(outcome.status, outcome.consumed, 0)
 
@@ -428,7 +487,8 @@ def validate(
 def count_device(op: int, src: torch.Tensor, *, stream: torch.cuda.Stream | None = None) -> torch.Tensor:
     """Enqueue a length (validate + count) or char-count op on a CUDA uint8
     tensor; returns the int64 result tensor (lu_outcome[3] for the length ops,
-    [1] count for the char counts).  No synchronisation."""
+    [1] count for the char counts).  No synchronisation (stream rules as
+    ``transcode_device``)."""
     srcb = _to_device_bytes(src, src.device)
     nbytes = srcb.numel()
     utf16 = op in (_native.OP_UTF8_LENGTH_FROM_UTF16LE, _native.OP_UTF16LE_CHAR_COUNT)
@@ -438,7 +498,9 @@ def count_device(op: int, src: torch.Tensor, *, stream: torch.cuda.Stream | None
     chars = op in (_native.OP_UTF8_CHAR_COUNT, _native.OP_UTF16LE_CHAR_COUNT)
     res = torch.empty(1 if chars else 3, dtype=torch.int64, device=srcb.device)
     ws = torch.empty(_native.workspace_bytes(op, n_units) // 8 + 1, dtype=torch.int64, device=srcb.device)
+    side = _side_stream(stream, srcb.device)
     _native.launch(op, srcb, n_units, None, 0, ws, res, stream)
+    _keep_alive(side, srcb if srcb.data_ptr() != src.data_ptr() else None, res, ws)
     return res
 
 

@@ -445,7 +445,8 @@ def test_kernels_on_pinned_host_buffers(cuda_ok, utf16):
 @pytest.mark.parametrize("utf16", [False, True])
 def test_config5_full_size_single_gpu(cuda_ok, utf16):
     """16 GiB of config-5 text (mixed profiles in seeded 64 MiB segments) on
-    one GPU: the UTF-8 <-> UTF-16 round trip is exact, and cutting the input
+    one GPU: the output equals the oracle's (segment by segment), the
+    UTF-8 <-> UTF-16 round trip is exact, and cutting the input
     at character boundaries into P = 2, 4, 8 shards, transcoding each shard
     separately and combining the per-shard records (the multi-GPU rule,
     shard.combine_records) reproduces the whole-buffer outcome and output."""
@@ -465,6 +466,24 @@ def test_config5_full_size_single_gpu(cuda_ok, utf16):
     o2 = outcome_from_tensor(res2.cpu())
     assert o2.ok and torch.equal(back.view(torch.uint8)[: src.numel()], src)
     del back, res2
+    # bit-exact against the oracle, segment by segment: segments end on
+    # character boundaries, so the whole-buffer output is the concatenation
+    # of the per-segment outputs (oracle.run_mt: all host threads)
+    import os
+
+    unit_in = 2 if utf16 else 1
+    op = oracle.OP_U16_U8 if utf16 else oracle.OP_U8_U16
+    pos = off = 0
+    for _name, _seed, seg_units in corpus.config5_segments(units, utf16=utf16):
+        seg = src[unit_in * pos: unit_in * (pos + seg_units)].cpu().numpy()
+        ref_out = np.empty(3 * seg_units if utf16 else seg_units, dtype=np.uint8 if utf16 else np.uint16)
+        st, consumed, wr = oracle.run_mt(op, seg, os.cpu_count() or 1, ref_out)
+        assert (st, consumed) == ("ok", seg_units)
+        got = payload[unit_out * off: unit_out * (off + wr)].cpu().numpy()
+        assert np.array_equal(got, ref_out.view(np.uint8)[: unit_out * wr]), (pos, off)
+        pos += seg_units
+        off += wr
+    assert (pos, off) == (units, whole.written)
     words = src.view(torch.int16) if utf16 else src
 
     def unit_at(i):
