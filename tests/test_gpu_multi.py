@@ -100,7 +100,7 @@ def test_sharded_native_two_ranks_gloo(cuda_ok, utf16):
                        start_method="spawn")
 
 
-def _nccl_world1(port: int) -> None:
+def _nccl_world1(_index: int, port: int) -> None:
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
