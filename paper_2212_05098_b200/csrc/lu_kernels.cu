@@ -226,6 +226,15 @@ constexpr int kPipeThreads = kGroupsPerCta * kGroupThreads;
 static_assert(kPipeThreads / 32 == kScanWarps, "CTA 0's warps are the scanner warps");
 
 constexpr int kMaxBufs = 3;
+// When a group takes its next tile ticket: 0 right after the tile-done
+// barrier (the atomic overlaps the combine), 1 at the top of the next
+// iteration after the resolve (default: a group never holds an unprocessed
+// tile while it waits on a prefix; K1 -1..-2%), 2 at the top before the
+// resolve (atomic and status poll overlap; neutral), 3 one iteration ahead
+// (K1 +6-24%: tiles held through resolve waits delay every later prefix).
+#ifndef LU_CLAIM_AT
+#define LU_CLAIM_AT 1
+#endif
 
 struct GroupShared {
     WarpResult wres[kMaxBufs][kGroupWarps];
@@ -401,8 +410,13 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     // group thread 0: the next tile; the ticket is taken right after the
     // tile-done barrier so its latency overlaps the combine + publish
     uint32_t next_claim = 0;
+#if LU_CLAIM_AT == 0 || LU_CLAIM_AT == 3
     if (gtid == 0)
         next_claim = atomicAdd(ticket, 1u);
+#endif
+#if LU_CLAIM_AT == 3
+    uint32_t pending_claim = 0;
+#endif
     for (;; ++i) {
         const uint32_t buf = i % kBufs;
         // Group thread 0 claims the next tile (atomic in flight) and resolves
@@ -411,9 +425,19 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
         // buffer, so the copy-out hides their latency.
         LU_T0();
         if (gtid == 0) {
+#if LU_CLAIM_AT == 2
+            next_claim = atomicAdd(ticket, 1u);
+#elif LU_CLAIM_AT == 3
+            if (i > 0)
+                next_claim = pending_claim;
+            pending_claim = atomicAdd(ticket, 1u); // consumed one iteration later
+#endif
             if (i >= kBufs)
                 pipe_resolve<Dir>(ps, buf, status, res, ntiles, lo_b, n_units, st_pre);
             LU_T(12); // resolve
+#if LU_CLAIM_AT == 1
+            next_claim = atomicAdd(ticket, 1u);
+#endif
             ps.claim = next_claim;
             // a tile after one that holds an error is never copied out and its
             // count is never used: skip its work (the reference stops at the
@@ -464,8 +488,10 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
             // combine the 4 warp results on lanes 0..3 (shallow dependency
             // chain: this is on the group's critical path)
             const uint32_t lane = gtid;
+#if LU_CLAIM_AT == 0
             if (lane == 0)
                 next_claim = atomicAdd(ticket, 1u);
+#endif
             const WarpResult r = ps.wres[buf][lane & (kGroupWarps - 1)];
             const uint32_t errm = __ballot_sync(0xffffffffu, lane < kGroupWarps && r.err);
             const uint32_t first = errm ? (uint32_t)__ffs(errm) - 1 : kGroupWarps;
