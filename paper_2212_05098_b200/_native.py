@@ -167,8 +167,22 @@ def _check(rc: int) -> None:
         raise RuntimeError(f"liblaneutf_b200: {kind}: {msg}")
 
 
-def _ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
-    return ctypes.c_void_p(t.data_ptr() if t is not None and t.numel() else 0)
+def _ptr(t: torch.Tensor | None) -> int:
+    return t.data_ptr() if t is not None and t.numel() else 0
+
+
+try:  # the raw cudaStream_t of the current stream without building a Stream object
+    _raw_stream = torch._C._cuda_getCurrentRawStream
+except AttributeError:  # pragma: no cover - older torch
+    _raw_stream = None
+
+
+def _stream_handle(stream, device: torch.device) -> int:
+    if stream is not None:
+        return stream.cuda_stream
+    if _raw_stream is not None:
+        return _raw_stream(device.index if device.index is not None else torch.cuda.current_device())
+    return torch.cuda.current_stream(device).cuda_stream
 
 
 def launch_batch(
@@ -183,8 +197,7 @@ def launch_batch(
     OP_VALIDATE_UTF8, OP_VALIDATE_UTF16LE): ``offsets`` is a CUDA int64 tensor
     of n_cases + 1 unit offsets into ``data``; ``res`` int64[n_cases, 3]."""
     L = lib()
-    s = stream if stream is not None else torch.cuda.current_stream(data.device)
-    sp = ctypes.c_void_p(s.cuda_stream)
+    sp = _stream_handle(stream, data.device)
     n = offsets.numel() - 1
     if op == OP_UTF8_TO_UTF16LE:
         rc = L.lu_batch_utf8_to_utf16le(_ptr(data), _ptr(offsets), n, _ptr(out), _ptr(res), sp)
@@ -216,8 +229,7 @@ def launch(
     uint64 count (``out`` unused).  Returns without synchronising.
     """
     L = lib()
-    s = stream if stream is not None else torch.cuda.current_stream(src.device)
-    sp = ctypes.c_void_p(s.cuda_stream)
+    sp = _stream_handle(stream, src.device)
     wsb = ws.numel() * ws.element_size()
     if op == OP_UTF8_TO_UTF16LE:
         rc = L.lu_utf8_to_utf16le(_ptr(src), n_units, _ptr(out), out_cap_units, _ptr(ws), wsb, _ptr(res), sp)

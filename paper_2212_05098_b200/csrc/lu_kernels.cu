@@ -360,11 +360,138 @@ __device__ __forceinline__ void pipe_copy(GroupShared &ps, uint32_t b, uint32_t 
                       ex + ps.warp_excl[b][wit] + out_lead);
 }
 
+// Warp 0 of a group, after the tile-done barrier: combine the 4 warp
+// results of buffer buf on lanes 0..3 (shallow dependency chain: this is on
+// the group's critical path) and publish the tile aggregate.
+__device__ __forceinline__ void group_combine(GroupShared &ps, uint32_t buf, uint32_t tile, uint64_t *status,
+                                              unsigned int *err_tile, uint32_t ntiles)
+{
+    const uint32_t lane = lane_id();
+    const WarpResult r = ps.wres[buf][lane & (kGroupWarps - 1)];
+    const uint32_t errm = __ballot_sync(0xffffffffu, lane < kGroupWarps && r.err);
+    const uint32_t first = errm ? (uint32_t)__ffs(errm) - 1 : kGroupWarps;
+    const uint32_t u = (lane < kGroupWarps && lane <= first) ? r.units : 0u;
+    uint32_t inc = u;
+    uint32_t o = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane >= 1)
+        inc += o;
+    o = __shfl_up_sync(0xffffffffu, inc, 2);
+    if (lane >= 2)
+        inc += o;
+    if (lane < kGroupWarps)
+        ps.warp_excl[buf][lane] = inc - u;
+    const uint32_t units = __shfl_sync(0xffffffffu, inc, kGroupWarps - 1);
+    if (lane == 0) {
+        ps.first_err[buf] = first;
+        ps.tile_of[buf] = tile;
+        ps.units[buf] = units;
+        // atomicMax: never overwrites a prefix (flag 2 > flag 1) that the
+        // scanner already published for a tile behind an error
+        atomicMax(reinterpret_cast<unsigned long long *>(&status[tile]),
+                  (unsigned long long)(kFlagAgg | (first < kGroupWarps ? kErrBit : 0ull) | (uint64_t)units));
+        if (first < kGroupWarps)
+            atomicMax(err_tile, ntiles - tile);
+    }
+}
+
+// Small inputs (ntiles <= 2 x resident CTAs, e.g. config 1's 4 MiB): every
+// group owns exactly one tile -- the CTA with role r (the r-th CTA to start)
+// takes tiles 2r and 2r+1 -- so there is no ticket, no scanner and no
+// deferred copy-out.  After publishing its aggregate the group sums the
+// aggregates of all earlier tiles itself (its 128 threads load them in
+// parallel; they belong to CTAs that started earlier, so the wait always
+// ends), then copies out.  Latency of a call drops from the persistent
+// pipeline's fill/drain chain to compute + one look-back.
+template <class Dir>
+__device__ __forceinline__ void small_tile(GroupShared &ps, uint32_t tile, uint32_t g, uint32_t wit, uint32_t gtid,
+                                           const uint8_t *__restrict__ base, int64_t lo_b, int64_t hi_b,
+                                           uint64_t n_units, typename Dir::OutT *out_g, typename Dir::OutT *out_a,
+                                           uint64_t out_lead, uint64_t *status, unsigned int *err_tile,
+                                           Outcome *res, uint32_t ntiles, const SelPair *sel,
+                                           unsigned long long *lb_sum, uint32_t *lb_err)
+{
+    const uint32_t bar_done = 2 + 3 * g, bar_prefix = 3 + 3 * g;
+    const int64_t tile_off = (int64_t)tile * kPipeTile;
+    const bool interior = (tile_off - 4 >= lo_b) && (tile_off + kPipeTile + 4 <= hi_b);
+    typename Dir::In in;
+    uint32_t hint = 2;
+    typename Dir::OutT *out_w = out_g + wit * Dir::kStride; // buffer 0
+    if (interior) {
+        Dir::template load<false>(base, tile_off, lo_b, hi_b, wit, in);
+        Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[0][wit], wit, in, hint);
+    } else {
+        Dir::template load<true>(base, tile_off, lo_b, hi_b, wit, in);
+        Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[0][wit], wit, in, hint);
+    }
+    bar_sync(bar_done, kGroupThreads);
+    if (wit == 0)
+        group_combine(ps, 0, tile, status, err_tile, ntiles);
+    // look-back: thread t of the group sums the aggregates of tiles j < tile
+    // with j = t (mod 128), loads issued 4 at a time
+    unsigned long long acc = 0;
+    uint32_t err = 0;
+    for (uint32_t j0 = gtid; j0 < tile; j0 += 4 * kGroupThreads) {
+        uint64_t v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t j = j0 + k * kGroupThreads;
+            v[k] = j < tile ? ld_acquire(&status[j]) : kFlagAgg;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t j = j0 + k * kGroupThreads;
+            uint32_t spins = 0;
+            uint64_t t0 = 0;
+            while ((v[k] >> kFlagShift) == 0) {
+                if (spins++ == 0)
+                    t0 = gtimer();
+                hang_check(spins, t0);
+                __nanosleep(32);
+                v[k] = ld_acquire(&status[j]);
+            }
+            acc += v[k] & kValMask;
+            err |= (v[k] & kErrBit) ? 1u : 0u;
+        }
+    }
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1)
+        acc += __shfl_xor_sync(0xffffffffu, acc, d);
+    err = __any_sync(0xffffffffu, err != 0);
+    if ((gtid & 31) == 0) {
+        lb_sum[wit] = acc;
+        lb_err[wit] = err;
+    }
+    bar_sync(bar_prefix, kGroupThreads);
+    if (gtid == 0) {
+        const unsigned long long sum = lb_sum[0] + lb_sum[1] + lb_sum[2] + lb_sum[3];
+        const bool e = (lb_err[0] | lb_err[1] | lb_err[2] | lb_err[3]) != 0;
+        const uint64_t ex = (sum & kValMask) | (e ? kErrBit : 0ull);
+        ps.excl[0] = ex;
+        if (!e) {
+            const uint32_t first = ps.first_err[0];
+            const uint64_t written = sum + ps.units[0];
+            if (first < kGroupWarps) {
+                res->status = kStatusMalformed;
+                res->pad = 0;
+                res->consumed = (uint64_t)((tile_off + ps.wres[0][first].pos - lo_b) >> Dir::kUnitShift);
+                res->written = written;
+            } else if (tile == ntiles - 1) {
+                res->status = kStatusOk;
+                res->pad = 0;
+                res->consumed = n_units;
+                res->written = written;
+            }
+        }
+    }
+    bar_sync(bar_prefix, kGroupThreads);
+    pipe_copy<Dir>(ps, 0, wit, out_g, out_a, out_lead);
+}
+
 template <class Dir>
 __global__ void __launch_bounds__(kPipeThreads, 3)
     k_transcode(const uint8_t *__restrict__ base, uint32_t lead, uint64_t n_units, uint64_t n_bytes,
                 typename Dir::OutT *__restrict__ out_a, uint32_t out_lead, uint64_t *__restrict__ status,
-                Outcome *__restrict__ res, uint32_t ntiles)
+                Outcome *__restrict__ res, uint32_t ntiles, uint32_t small)
 {
     using OutT = typename Dir::OutT;
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -372,6 +499,8 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     __shared__ GroupShared gshared[kGroupsPerCta];
     __shared__ ScanShared scan_s;
     __shared__ uint32_t role_s;
+    __shared__ unsigned long long lb_sum[kGroupsPerCta][kGroupWarps];
+    __shared__ uint32_t lb_err[kGroupsPerCta][kGroupWarps];
 
     const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n_bytes;
     unsigned int *ticket = reinterpret_cast<unsigned int *>(status + ntiles);
@@ -391,6 +520,15 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     __syncthreads();
     const uint32_t warp = threadIdx.x >> 5;
     LU_PROF_INIT();
+    if (small) {
+        const uint32_t g = warp / kGroupWarps, wit = warp % kGroupWarps;
+        const uint32_t tile = role_s * kGroupsPerCta + g;
+        if (tile < ntiles)
+            small_tile<Dir>(gshared[g], tile, g, wit, threadIdx.x - g * kGroupThreads, base, lo_b, hi_b, n_units,
+                            reinterpret_cast<OutT *>(smem_raw) + g * (Dir::kBufs * kGroupWarps * Dir::kStride), out_a,
+                            out_lead, status, err_tile, res, ntiles, sel, lb_sum[g], lb_err[g]);
+        return;
+    }
     if (role_s == 0) {
         scan_windows<Dir::kScanPerLane>(status, ntiles, warp, scan_s);
         LU_PROF_FLUSH();
@@ -485,38 +623,11 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
         LU_T(5); // tile-done barrier wait
         LU_CNT(6, 1);
         if (wit == 0) {
-            // combine the 4 warp results on lanes 0..3 (shallow dependency
-            // chain: this is on the group's critical path)
-            const uint32_t lane = gtid;
 #if LU_CLAIM_AT == 0
-            if (lane == 0)
+            if (gtid == 0)
                 next_claim = atomicAdd(ticket, 1u);
 #endif
-            const WarpResult r = ps.wres[buf][lane & (kGroupWarps - 1)];
-            const uint32_t errm = __ballot_sync(0xffffffffu, lane < kGroupWarps && r.err);
-            const uint32_t first = errm ? (uint32_t)__ffs(errm) - 1 : kGroupWarps;
-            const uint32_t u = (lane < kGroupWarps && lane <= first) ? r.units : 0u;
-            uint32_t inc = u;
-            uint32_t o = __shfl_up_sync(0xffffffffu, inc, 1);
-            if (lane >= 1)
-                inc += o;
-            o = __shfl_up_sync(0xffffffffu, inc, 2);
-            if (lane >= 2)
-                inc += o;
-            if (lane < kGroupWarps)
-                ps.warp_excl[buf][lane] = inc - u;
-            const uint32_t units = __shfl_sync(0xffffffffu, inc, kGroupWarps - 1);
-            if (lane == 0) {
-                ps.first_err[buf] = first;
-                ps.tile_of[buf] = tile;
-                ps.units[buf] = units;
-                // atomicMax: never overwrites a prefix (flag 2 > flag 1) that the
-                // scanner already published for a tile behind an error
-                atomicMax(reinterpret_cast<unsigned long long *>(&status[tile]),
-                          (unsigned long long)(kFlagAgg | (first < kGroupWarps ? kErrBit : 0ull) | (uint64_t)units));
-                if (first < kGroupWarps)
-                    atomicMax(err_tile, ntiles - tile);
-            }
+            group_combine(ps, buf, tile, status, err_tile, ntiles);
         }
         LU_T(7); // combine + publish
     }
@@ -911,18 +1022,54 @@ static int set_smem_attrs()
 
 // Grid of a persistent pipelined kernel: every CTA must be resident (tiles
 // wait on smaller tiles held by other CTAs), so never exceed the occupancy.
-static int persistent_grid(const void *fn, int threads, size_t smem, uint64_t ntiles, unsigned *grid,
-                           unsigned extra = 0)
+// Resident capacity (SMs x CTAs per SM) of a kernel configuration, cached per
+// device: the occupancy query costs several microseconds of host time per
+// call, which dominated small calls (config 1).
+struct CapEntry {
+    int dev;
+    const void *fn;
+    int threads;
+    size_t smem;
+    uint64_t cap;
+};
+static std::mutex g_cap_mu;
+static CapEntry g_cap[64];
+static int g_ncap = 0;
+
+static int resident_capacity(const void *fn, int threads, size_t smem, uint64_t *cap)
 {
-    int dev = 0, sms = 0, per_sm = 0;
+    int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
-    if (e == cudaSuccess)
-        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess)
+        return cuda_fail(e, "cudaGetDevice");
+    {
+        std::lock_guard<std::mutex> lock(g_cap_mu);
+        for (int k = 0; k < g_ncap; ++k)
+            if (g_cap[k].dev == dev && g_cap[k].fn == fn && g_cap[k].threads == threads && g_cap[k].smem == smem) {
+                *cap = g_cap[k].cap;
+                return 0;
+            }
+    }
+    int sms = 0, per_sm = 0;
+    e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess)
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
     if (e != cudaSuccess)
         return cuda_fail(e, "occupancy query");
-    const uint64_t cap = (uint64_t)sms * (uint64_t)per_sm;
+    *cap = (uint64_t)sms * (uint64_t)per_sm;
+    std::lock_guard<std::mutex> lock(g_cap_mu);
+    if (g_ncap < 64)
+        g_cap[g_ncap++] = CapEntry{dev, fn, threads, smem, *cap};
+    return 0;
+}
+
+// Grid of a persistent kernel: never more CTAs than are resident at once.
+static int persistent_grid(const void *fn, int threads, size_t smem, uint64_t ntiles, unsigned *grid,
+                           unsigned extra = 0)
+{
+    uint64_t cap = 0;
+    if (int rc = resident_capacity(fn, threads, smem, &cap))
+        return rc;
     if (cap < 1 + extra)
         return fail(LU_ERR_CUDA, "persistent kernel cannot be resident on this device");
     // extra: CTAs that process no tiles (the transcode kernels' scanner CTA)
@@ -1052,12 +1199,18 @@ static int u8u16_impl(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint64
     const uint32_t out_lead = (uint32_t)(((uintptr_t)out_safe & 15) >> 1);
     uint16_t *out_a = out_safe - out_lead;
     unsigned grid = 0;
-    rc = persistent_grid((const void *)k_transcode<Dir>, kPipeThreads, kSmemK1, nt, &grid, 1);
+    uint64_t cap = 0;
+    rc = resident_capacity((const void *)k_transcode<Dir>, kPipeThreads, kSmemK1, &cap);
     if (rc)
         return rc;
+    const uint32_t small = nt <= kGroupsPerCta * cap ? 1u : 0u; // one tile per group: no scanner
+    grid = small ? (unsigned)((nt + kGroupsPerCta - 1) / kGroupsPerCta) : (unsigned)(nt + 1 < cap ? nt + 1 : cap);
+    if (!small && cap < 2)
+        return fail(LU_ERR_CUDA, "persistent kernel cannot be resident on this device");
     k_transcode<Dir><<<grid, kPipeThreads, kSmemK1, stream>>>(base, lead, n_bytes, n_bytes, out_a, out_lead,
                                                                    reinterpret_cast<uint64_t *>(ws),
-                                                                   reinterpret_cast<Outcome *>(res), (uint32_t)nt);
+                                                                   reinterpret_cast<Outcome *>(res), (uint32_t)nt,
+                                                                   small);
     e = cudaGetLastError();
     if (e != cudaSuccess)
         return cuda_fail(e, "k_utf8_to_utf16le launch");
@@ -1093,12 +1246,17 @@ static int u16u8_impl(const uint16_t *in, uint64_t n_words, uint8_t *out, uint64
     uint8_t *out_safe = out ? out : reinterpret_cast<uint8_t *>(16);
     const uint32_t out_lead = (uint32_t)((uintptr_t)out_safe & 15);
     unsigned grid = 0;
-    rc = persistent_grid((const void *)k_transcode<Dir>, kPipeThreads, kSmemK2, nt, &grid, 1);
+    uint64_t cap = 0;
+    rc = resident_capacity((const void *)k_transcode<Dir>, kPipeThreads, kSmemK2, &cap);
     if (rc)
         return rc;
+    const uint32_t small = nt <= kGroupsPerCta * cap ? 1u : 0u; // one tile per group: no scanner
+    grid = small ? (unsigned)((nt + kGroupsPerCta - 1) / kGroupsPerCta) : (unsigned)(nt + 1 < cap ? nt + 1 : cap);
+    if (!small && cap < 2)
+        return fail(LU_ERR_CUDA, "persistent kernel cannot be resident on this device");
     k_transcode<Dir><<<grid, kPipeThreads, kSmemK2, stream>>>(
         base, lead, n_words, 2 * n_words, out_safe - out_lead, out_lead, reinterpret_cast<uint64_t *>(ws),
-        reinterpret_cast<Outcome *>(res), (uint32_t)nt);
+        reinterpret_cast<Outcome *>(res), (uint32_t)nt, small);
     e = cudaGetLastError();
     if (e != cudaSuccess)
         return cuda_fail(e, "k_utf16le_to_utf8 launch");

@@ -227,6 +227,9 @@ def _byte_len(data) -> int:
 
 def _to_device_bytes(data, device: torch.device) -> torch.Tensor:
     """Input as a contiguous uint8 CUDA tensor (zero-copy when already there)."""
+    if (type(data) is torch.Tensor and data.is_cuda and data.dtype == torch.uint8 and data.dim() == 1
+            and data.is_contiguous() and data.get_device() == device.index):
+        return data  # fast path: nothing to convert (small calls are host-bound)
     if isinstance(data, torch.Tensor):
         t = data.contiguous()
         if t.dtype != torch.uint8:
