@@ -45,9 +45,18 @@
  *     per UTF-16 word).  Exactly out[0 .. written) is written; nothing past
  *     it (the reference's canary contract).
  *   - ``ws`` is caller-owned device scratch of at least
- *     lu_workspace_bytes(op, n_units) bytes, 8-byte aligned; the library
- *     allocates nothing and holds no mutable global state.  One workspace
- *     must not be shared by calls that may run concurrently.
+ *     lu_workspace_bytes(op, n_units) bytes, 8-byte aligned, any contents
+ *     (each call zeroes what it uses on its stream); the library allocates
+ *     nothing.  Its only global state is a mutex-protected per-device cache
+ *     (kernel attributes, resident capacity).  One workspace must not be
+ *     shared by calls that may run concurrently; calls on disjoint buffers
+ *     may run concurrently on any streams and threads.
+ *   - Concurrency with other kernels: the transcode kernels are persistent
+ *     (grid <= resident capacity) but do NOT require their CTAs to be
+ *     co-resident -- the tile-ordering scanner is the first CTA to start and
+ *     every wait is on work claimed by running CTAs -- so they make progress
+ *     when other work holds SMs.  A spin-wait that sees no progress for 10 s
+ *     of GPU time traps (a launch error) rather than hanging.
  *   - Return value 0 = enqueued; negative = error, message in lu_last_error()
  *     (thread-local).  Malformed input is NOT an error: it is a status.
  */

@@ -4,7 +4,9 @@
 // walks it in 4 rounds of 512 B, lane l holding bytes [16l, 16l+16) of the
 // round in registers (neighbours by shuffle).  The transcode kernels group 4
 // chunks into an 8 KiB tile; tiles are ordered by the central scanner
-// (scan_windows, the warps of CTA 0) rather than a per-tile look-back.
+// (scan_windows, the warps of the first CTA to start) rather than a per-tile
+// look-back; inputs of at most two tiles per resident CTA use one tile per
+// group and an in-group look-back instead (small_tile).
 //
 // Tile status word (uint64, one per tile, zeroed before each launch):
 //   bits 63..62  flag: 0 not ready, 1 aggregate, 2 exclusive prefix
@@ -28,8 +30,8 @@ enum : int32_t { kStatusOk = 0, kStatusMalformed = 1, kStatusOutputTooSmall = 2 
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kTileBytes = 16384;
-constexpr int kChunkBytes = kTileBytes / kWarps;      // 2048 B per warp
+constexpr int kChunkBytes = 2048;                     // input bytes per warp chunk
+constexpr int kTileBytes = kWarps * kChunkBytes;      // 16 KiB: a CTA's chunks (validators' tile count)
 
 constexpr uint32_t H8 = 0x80808080u;
 
@@ -163,7 +165,8 @@ __shared__ unsigned long long s_prof[10][24]; // [warp][counter], lane 0 only
 #define LU_PROF_FLUSH()
 #endif
 
-// Central scanner: the kScanWarps warps of CTA 0 (which computes no tiles).
+// Central scanner: the kScanWarps warps of the first CTA to start (which
+// computes no tiles).
 // Tiles publish only their aggregate (flag 1).  Scanner warp k owns the
 // fixed windows k, k + kScanWarps, ... of kScanWindow tiles (lane l holds
 // tiles [4l, 4l+4) of a window).  It takes the window base from the previous

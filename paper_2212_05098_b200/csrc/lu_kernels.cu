@@ -235,6 +235,9 @@ constexpr int kMaxBufs = 3;
 #ifndef LU_CLAIM_AT
 #define LU_CLAIM_AT 1
 #endif
+#ifndef LU_RESOLVE_SLEEP
+#define LU_RESOLVE_SLEEP 32 // ns between polls of a tile's status word
+#endif
 
 struct GroupShared {
     WarpResult wres[kMaxBufs][kGroupWarps];
@@ -322,7 +325,7 @@ __device__ __forceinline__ void pipe_resolve(GroupShared &ps, uint32_t b, uint64
     uint32_t spins = 0;
     const uint64_t t0 = (st >> kFlagShift) != 2 ? gtimer() : 0;
     while ((st >> kFlagShift) != 2) {
-        __nanosleep(32);
+        __nanosleep(LU_RESOLVE_SLEEP);
         st = ld_acquire(&status[tile]);
         ++spins;
         hang_check(spins, t0);

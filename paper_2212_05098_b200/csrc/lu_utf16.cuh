@@ -6,8 +6,9 @@
 // preceded by a high one -- an exact local predicate, so
 // the detector IS the exact check here.  Output bytes per word: 1 (< 0x80),
 // 2 (< 0x800), 3 (other non-surrogates), 4 for a high surrogate that starts a
-// pair, 0 for the low surrogate that ends one.  A lane holds one 32-bit quad
-// = two words; a 128-byte warp step covers 64 words.
+// pair, 0 for the low surrogate that ends one.  Work layout as on the UTF-8
+// side: a warp walks its 2 KiB chunk in 512-byte rounds, lane l holding 16
+// bytes (8 words, four 32-bit quads of two words each) per round.
 #pragma once
 
 #include "lu_common.cuh"
