@@ -388,7 +388,8 @@ def config5_sharded(utf16: bool, world: int, rank: int, dev: torch.device, peak:
     stream = torch.cuda.current_stream(dev)
     res, out = transcode_device(direction, shard)
     if world > 1:
-        bounds = torch.tensor([begin, end], dtype=torch.int64, device=dev)
+        bdev = dev if dist.get_backend() == "nccl" else torch.device("cpu")
+        bounds = torch.tensor([begin, end], dtype=torch.int64, device=bdev)
         allb = [torch.empty_like(bounds) for _ in range(world)]
         dist.all_gather(allb, bounds)
         allb = [t.tolist() for t in allb]
@@ -417,7 +418,7 @@ def config5_sharded(utf16: bool, world: int, rank: int, dev: torch.device, peak:
     torch.cuda.synchronize()
     t = a.elapsed_time(b) / 1e3 / steps
     if world > 1:
-        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t], dtype=torch.float64, device=bdev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
         dist.barrier()

@@ -110,8 +110,10 @@ def transcode_sharded(
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    mine = torch.empty(4, dtype=torch.int64, device=local_record.device)
-    mine[:3] = local_record.view(torch.int64)[:3]
+    # NCCL gathers device tensors; gloo (CPU tests) needs host tensors
+    dev = local_record.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    mine = torch.empty(4, dtype=torch.int64, device=dev)
+    mine[:3] = local_record.view(torch.int64)[:3].to(dev)
     mine[3] = begin
     gathered = [torch.empty_like(mine) for _ in range(world)]
     dist.all_gather(gathered, mine, group=group)

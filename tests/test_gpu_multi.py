@@ -143,3 +143,37 @@ def test_bench_config5_sharded_one_rank(cuda_ok):
         r = bench.config5_sharded(utf16, 1, 0, dev, 6552.0, steps=1)
         assert r["ok"], r
         assert r["consumed"] == (16 << 30) // (2 if utf16 else 1)
+
+
+def _bench_c5_rank(rank: int, world: int, port: int, utf16: bool, q) -> None:
+    import bench
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        r = bench.config5_sharded(utf16, world, rank, torch.device("cuda", 0), 6552.0, steps=1)
+        if rank == 0:
+            q.put(r)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(1200)
+@pytest.mark.parametrize("utf16", [False, True])
+def test_bench_config5_sharded_two_ranks(cuda_ok, utf16):
+    """The multi-GPU bench's config-5 step at world size 2 (both ranks on
+    cuda:0, gloo for the records): each rank builds only its half of the
+    16 GiB input, the two cuts agree, and the combined outcome equals the
+    one-rank run (valid, complete, same written count)."""
+    import bench
+
+    one = bench.config5_sharded(utf16, 1, 0, torch.device("cuda", 0), 6552.0, steps=1)
+    torch.cuda.empty_cache()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_bench_c5_rank, args=(2, _free_port(), utf16, q), nprocs=2, join=True, start_method="spawn")
+    two = q.get(timeout=10)
+    assert two["ok"] and one["ok"], (one, two)
+    assert (two["status"], two["consumed"], two["written"]) == (one["status"], one["consumed"], one["written"])
+    assert two["n_gpus"] == 2 and two["rank0_local_written"] < one["written"]
