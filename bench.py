@@ -50,7 +50,7 @@ PROFILES = (("latin", 1), ("cyrillic", 2), ("cjk", 3), ("emoji", 4))
 BUF_BYTES = 256 << 20
 METRIC = "input GiB/s transcoded+validated (device-timed) and % of HBM roofline"
 GIB = float(1 << 30)
-EV_EVERY = 8  # steps of the timed region that carry per-launch timing events
+EV_EVERY = 4  # steps of the timed region that carry per-launch timing events
 REF_BUDGET_S = 150.0  # --impl reference: bound on the timed CPU run
 WORKLOAD = ("config2: UTF-8->UTF-16LE, 4 x 256 MiB valid buffers per GPU "
             "(latin/cyrillic/cjk/emoji, seeds 1-4 (+100*rank))")
