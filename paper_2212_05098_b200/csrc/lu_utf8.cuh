@@ -29,6 +29,13 @@
 
 #include <type_traits>
 
+#ifndef LU_ONE_VOTE
+#define LU_ONE_VOTE 1
+#endif
+#ifndef LU_MERGED_TERMS
+#define LU_MERGED_TERMS 1
+#endif
+
 namespace lu {
 
 struct U8Masks {
@@ -283,8 +290,13 @@ __device__ __forceinline__ uint32_t u8_fast0(U8Round &R)
         const uint32_t t1 = x << 1;
         const uint32_t C = x & ~t1 & H8, L = x & t1 & H8;
         det |= fsl(Lp, L, 8) ^ C;                          // continuation structure
+#if LU_MERGED_TERMS
+        // a lead >= E0 (not this class) or C0 / C1: one LOP3 per term pair
+        det |= L & ((x << 2) | ~((x & 0x1E1E1E1Eu) + 0x7F7F7F7Fu));
+#else
         det |= L & (x << 2);                               // a lead >= E0: not this class
         det |= L & ~((x & 0x1E1E1E1Eu) + 0x7F7F7F7Fu);      // C0 / C1
+#endif
         R.m[k].C = C;
         R.m[k].L = L;
         R.m[k].E = 0;
@@ -313,10 +325,16 @@ __device__ __forceinline__ uint32_t u8_fast1(U8Round &R)
         const uint32_t need = E * 0x10100u + spill;        // E(i-1) | E(i-2)
         spill = __umulhi(E, 0x10100u);
         det |= need ^ C;
+        const uint32_t v = x + 0x03030303u;                // E0 / ED candidates (u8_prefilter_e)
+#if LU_MERGED_TERMS
+        // a 2-byte lead, an F-class byte, or an E0 / ED candidate: with
+        // E = L & t2, L & ~t2 | E & (x3 | ~v4 & ~v5) = L & (~t2 | x3 | ~(v4 | v5))
+        det |= L & (~t2 | (x << 3) | ~((v << 4) | (v << 5)));
+#else
         det |= L & ~t2;                                    // a 2-byte lead: not this class
         det |= E & (x << 3);                               // an F-class byte: not this class
-        const uint32_t v = x + 0x03030303u;                // E0 / ED candidates (u8_prefilter_e)
         det |= E & ~(v << 4) & ~(v << 5);
+#endif
         R.m[k].C = C;
         R.m[k].L = E;
         R.m[k].E = E;
@@ -671,13 +689,21 @@ __device__ __forceinline__ uint32_t u8u16_chunk_fast(const uint8_t *__restrict__
         uint32_t fd = P == 0 ? u8_fast0(R) : P == 1 ? u8_fast1(R) : u8_fast3(R);
         if (r == kRounds - 1 && lane == 31)
             fd |= u8_chunk_end_check(R);
+#if LU_ONE_VOTE
+        miss |= fd; // one vote for the chunk, below
+#else
         miss |= __any_sync(0xffffffffu, fd != 0) ? 1u : 0u;
+#endif
         R.path = P;
         R.det = 0;
         u8u16_round<P, false, BE>(R, r, base, tile_off, chunk, lane_off, lo_b, hi_b, sbase, sel, running, err,
                                   err_pos, units);
     }
+#if LU_ONE_VOTE
+    return __any_sync(0xffffffffu, miss != 0) ? 1u : 0u;
+#else
     return miss;
+#endif
 }
 
 template <bool Boundary, bool BE = false>
@@ -814,7 +840,11 @@ __device__ __forceinline__ void u8val_warp_in(const uint8_t *__restrict__ base, 
             uint32_t fd = P == 3 ? u8_fast3(R) : (hint == 0 ? u8_fast0(R) : u8_fast1(R));
             if (r == kRounds - 1 && lane == 31)
                 fd |= u8_chunk_end_check(R);
+#if LU_ONE_VOTE
+            miss |= fd;
+#else
             miss |= __any_sync(0xffffffffu, fd != 0) ? 1u : 0u;
+#endif
             if (Count) {
 #pragma unroll
                 for (int k = 1; k <= 4; ++k)
@@ -822,7 +852,11 @@ __device__ __forceinline__ void u8val_warp_in(const uint8_t *__restrict__ base, 
                                  : (~R.m[k].C & H8) >> 7; // no F bytes in paths 0 / 1
             }
         }
+#if LU_ONE_VOTE
+        if (__any_sync(0xffffffffu, miss != 0))
+#else
         if (miss)
+#endif
             return false;
         if (lane == 0) {
             wr.err = 0;
