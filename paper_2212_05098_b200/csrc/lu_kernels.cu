@@ -15,6 +15,7 @@
 #include "lu_common.cuh"
 #include "lu_utf16.cuh"
 #include "lu_utf8.cuh"
+#include "lu_utf8_lc.cuh"
 
 #include "../../include/laneutf_b200.h"
 
@@ -666,6 +667,13 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
 // The last warp to finish writes the result record.
 // ws layout: [u64 max(n - bad_pos)][u32 warps done][u32 pad][u64 count].
 
+#ifndef LU_LC_CTAS
+#define LU_LC_CTAS 3 // resident CTAs per SM the lane-contiguous validator is compiled for
+#endif
+#ifndef LU_K3_LC
+#define LU_K3_LC 1 // UTF-8 validation / length through k_validate8_lc
+#endif
+
 constexpr int kValStages = 2;
 constexpr int kValCPW = 2;                                   // chunks per warp per stage
 constexpr int kStageBytes = kWarps * kValCPW * kChunkBytes; // 32 KiB
@@ -808,6 +816,250 @@ __global__ void __launch_bounds__(kThreads, 3) k_validate_w(const uint8_t *__res
     }
     if (Count) {
         const uint32_t wsum = __reduce_add_sync(0xffffffffu, count);
+        if (lane == 0 && wsum)
+            atomicAdd(reinterpret_cast<unsigned long long *>(ws + 2), (unsigned long long)wsum);
+    }
+    if (lane == 0) {
+        __threadfence();
+        const unsigned int prev = atomicAdd(reinterpret_cast<unsigned int *>(ws + 1), 1u);
+        if (prev == total_warps - 1) {
+            __threadfence();
+            const uint64_t b = atomicAdd(reinterpret_cast<unsigned long long *>(ws), 0ull);
+            res->status = b ? kStatusMalformed : kStatusOk;
+            res->pad = 0;
+            res->consumed = n - b;
+            res->written = (Count && !b) ? atomicAdd(reinterpret_cast<unsigned long long *>(ws + 2), 0ull) : 0;
+        }
+    }
+}
+
+// ============================================== K3 (lane-contiguous layout)
+//
+// validate_utf8 / utf16_length_from_utf8 with the lane-contiguous detectors of
+// lu_utf8_lc.cuh.  No CTA-wide step: every warp owns a private ring of
+// kLcSlots slots (one 2 KiB chunk plus 16 bytes of look-behind / look-ahead
+// each) that its lane 0 keeps filled with TMA bulk copies (one mbarrier per
+// slot); warp g of G takes chunks g, g + G, ...  Lane l reads its 64 bytes
+// with four LDS.128 and runs the detector of the warp's predicted class over
+// its 16 quads in a straight line; one vote per chunk.  A miss falls to the
+// exact general detector on the same registers; only a chunk that detector
+// flags (a real error) or a chunk at the ends of the input goes through the
+// round-layout code (u8val_warp_in), which owns the error offsets.
+// ws layout and result protocol as k_validate_w.
+
+#ifndef LU_LC_SUB
+#define LU_LC_SUB 2 // chunks per ring slot (one TMA bulk copy, one stop check, one refill per slot)
+#endif
+#ifndef LU_LC_SLOTS
+#define LU_LC_SLOTS 2
+#endif
+constexpr int kLcSub = LU_LC_SUB;
+constexpr int kLcSlots = LU_LC_SLOTS;
+constexpr int kLcHalo = 16;
+constexpr int kLcSuper = kLcSub * kChunkBytes;           // input bytes per slot
+constexpr int kLcSlotBytes = kLcSuper + 2 * kLcHalo;
+constexpr size_t kSmemLc = (size_t)kWarps * kLcSlots * kLcSlotBytes;
+
+__device__ __forceinline__ uint4 lds128(uint32_t a)
+{
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+// Round-layout fallback for one chunk: from the ring slot (sa = shared address
+// of the chunk's first byte) when the chunk is interior, else masked global
+// loads.  Out of line: it is rare and must not shape the fast path's registers.
+// Returns the new class hint << 32 | this lane's share of the chunk's count.
+template <bool Count>
+__device__ __noinline__ uint64_t lc_slow_chunk(const uint8_t *__restrict__ base, int64_t off, int64_t lo_b,
+                                               int64_t hi_b, uint32_t sa, bool interior, WarpResult *wr, uint32_t hint)
+{
+    const uint32_t lane = lane_id();
+    ChunkIn in;
+    uint32_t c = 0;
+    if (interior) {
+#pragma unroll
+        for (int r = 0; r < kChunkBytes / 512; ++r)
+            in.q[r] = lds128(sa + r * 512 + 16 * lane);
+        in.halo_p = lds32(sa - 4);
+        in.halo_n = lds32(sa + kChunkBytes);
+        u8val_warp_in<false, Count>(base, off, lo_b, hi_b, in, *wr, 0, hint, &c);
+    } else {
+        load_chunk<true>(base, off, lo_b, hi_b, in);
+        u8val_warp_in<true, Count>(base, off, lo_b, hi_b, in, *wr, 0, hint, &c);
+    }
+    return ((uint64_t)hint << 32) | c;
+}
+
+// Lane l's 64 bytes of the chunk at shared address sa, plus the quads before /
+// after them (previous / next lane, or the slot's halo for lanes 0 / 31).
+__device__ __forceinline__ void lc_load(uint32_t sa, uint32_t lane, uint32_t (&x)[kLcQuads], uint32_t &xp,
+                                        uint32_t &xn)
+{
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint4 v = lds128(sa + 64 * lane + 16 * j);
+        x[4 * j] = v.x;
+        x[4 * j + 1] = v.y;
+        x[4 * j + 2] = v.z;
+        x[4 * j + 3] = v.w;
+    }
+    const uint32_t hp = lds32(sa - 4), hn = lds32(sa + kChunkBytes);
+    xp = __shfl_up_sync(0xffffffffu, x[kLcQuads - 1], 1);
+    xn = __shfl_down_sync(0xffffffffu, x[0], 1);
+    xp = lane == 0 ? hp : xp;
+    xn = lane == 31 ? hn : xn;
+}
+
+template <bool Count>
+__global__ void __launch_bounds__(kThreads, LU_LC_CTAS) k_validate8_lc(const uint8_t *__restrict__ base, uint32_t lead,
+                                                                       uint64_t n, uint64_t *__restrict__ ws,
+                                                                       Outcome *__restrict__ res, uint32_t nsuper)
+{
+    extern __shared__ __align__(128) uint8_t ring[];
+    __shared__ __align__(8) uint64_t bar[kWarps * kLcSlots];
+    __shared__ WarpResult wr_s[kWarps];
+    __shared__ __align__(8) uint64_t best_s[kWarps];
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t lane = lane_id();
+    const uint32_t total_warps = gridDim.x * kWarps;
+    const uint32_t gw = blockIdx.x * kWarps + warp;
+    const uint32_t best_a = (uint32_t)__cvta_generic_to_shared(&best_s[warp]);
+    const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n;
+    // slots (kLcSub consecutive chunks) whose +-16-byte window lies inside
+    // [lo, hi) come through the ring: [1, s_hi) (lead < 16: slot 0 never does)
+    const uint32_t s_hi = hi_b >= kLcSuper + kLcHalo ? (uint32_t)((hi_b - kLcHalo) / kLcSuper) : 0u;
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bar[warp * kLcSlots]);
+    const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(ring) + warp * (kLcSlots * kLcSlotBytes);
+    auto issue = [&](uint32_t sc, uint32_t slot) {
+        const uint32_t b = bar0 + 8 * slot;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kLcSlotBytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         ring0 + slot * kLcSlotBytes),
+                     "l"(base + (int64_t)sc * kLcSuper - kLcHalo), "r"(kLcSlotBytes), "r"(b)
+                     : "memory");
+    };
+    if (lane == 0) {
+        for (int k = 0; k < kLcSlots; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * k));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    if (lane == 0)
+        for (uint32_t k = 0; k < (uint32_t)kLcSlots; ++k) {
+            const uint32_t sc = gw + k * total_warps;
+            if (sc >= 1 && sc < s_hi)
+                issue(sc, k);
+        }
+    uint32_t hint = 2;   // the warp's class prediction (0, 1, 3; 2 = general)
+    uint32_t units = 0;  // Count: this lane's output units over the warp's chunks
+    uint32_t parity = 0; // bit k: mbarrier phase of ring slot k
+    uint32_t slot = 0;
+    uint32_t sc = gw;
+    bool stopped = false;
+    for (; sc < nsuper; sc += total_warps) {
+        const bool fast = sc >= 1 && sc < s_hi;
+        // published first-error position: fetched now into shared memory
+        // (cp.async: no register held across the chunks), read after them
+        if (lane == 0)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n\tcp.async.commit_group;" ::"r"(best_a), "l"(ws)
+                         : "memory");
+        const uint32_t sa0 = ring0 + slot * kLcSlotBytes + kLcHalo;
+        if (fast) {
+            mbar_wait(bar0 + 8 * slot, (parity >> slot) & 1);
+            parity ^= 1u << slot;
+        }
+        uint32_t err = 0;
+#pragma unroll 1
+        for (int h = 0; h < kLcSub; ++h) {
+            const int64_t off = (int64_t)sc * kLcSuper + h * kChunkBytes;
+            if (off >= hi_b)
+                break;
+            const uint32_t sa = sa0 + h * kChunkBytes;
+            bool slow = !fast;
+            if (fast) {
+                uint32_t x[kLcQuads], xp, xn;
+                lc_load(sa, lane, x, xp, xn);
+                uint32_t fd = 1, c_nc = 0, c_nf = 0;
+                if (hint == 0)
+                    fd = lc_detect<0, Count>(x, xp, xn, c_nc, c_nf);
+                else if (hint == 1)
+                    fd = lc_detect<1, Count>(x, xp, xn, c_nc, c_nf);
+                else if (hint == 3)
+                    fd = lc_detect<3, Count>(x, xp, xn, c_nc, c_nf);
+                if (__any_sync(0xffffffffu, fd != 0)) {
+                    // class miss: the exact general detector on the same registers
+                    uint32_t cls = 0;
+                    c_nc = 0;
+                    c_nf = 0;
+                    fd = lc_detect_general<Count>(x, xp, xn, c_nc, c_nf, cls);
+                    hint = lc_path_of(__reduce_or_sync(0xffffffffu, cls));
+                    slow = __any_sync(0xffffffffu, fd != 0);
+                }
+                // 64 bytes per lane minus continuations plus 4-byte leads
+                if (Count && !slow)
+                    units += 64u - (c_nc >> 7) + (c_nf >> 7);
+            }
+            if (slow) {
+                const uint64_t hc = lc_slow_chunk<Count>(base, off, lo_b, hi_b, sa, fast, &wr_s[warp], hint);
+                hint = (uint32_t)(hc >> 32);
+                __syncwarp();
+                err = wr_s[warp].err;
+                const uint32_t pos = wr_s[warp].pos;
+                __syncwarp();
+                if (Count)
+                    units += (uint32_t)hc; // this lane's share of the chunk's count (u8val_warp_in)
+                if (err) {
+                    if (lane == 0) {
+                        const uint64_t pu = (uint64_t)(off + pos - lo_b);
+                        atomicMax(reinterpret_cast<unsigned long long *>(ws), (unsigned long long)(n - pu));
+                    }
+                    break;
+                }
+            }
+        }
+        __syncwarp(); // every lane is done with the slot
+        // stop once an error is known before this warp's next slot
+        uint32_t stop = err;
+        if (lane == 0) {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            uint64_t best;
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(best) : "r"(best_a) : "memory");
+            if (best != 0)
+                stop |= (uint64_t)(hi_b - (int64_t)best) < (uint64_t)(sc + total_warps) * kLcSuper ? 1u : 0u;
+        }
+        if (__shfl_sync(0xffffffffu, stop, 0)) {
+            stopped = true;
+            break;
+        }
+        if (lane == 0) {
+            const uint32_t sn = sc + kLcSlots * total_warps;
+            if (sn < s_hi && sn >= 1)
+                issue(sn, slot);
+        }
+        slot = slot == kLcSlots - 1 ? 0u : slot + 1;
+    }
+    // an early stop leaves up to kLcSlots - 1 slots in flight: let them land
+    // before the CTA (and its shared memory) goes away
+    if (stopped) {
+        for (uint32_t d = 1; d < (uint32_t)kLcSlots; ++d) {
+            const uint64_t sd = (uint64_t)sc + (uint64_t)d * total_warps;
+            slot = slot == kLcSlots - 1 ? 0u : slot + 1;
+            if (sd >= 1 && sd < s_hi) {
+                mbar_wait(bar0 + 8 * slot, (parity >> slot) & 1);
+                parity ^= 1u << slot;
+            }
+        }
+    }
+    if (Count) {
+        const uint32_t wsum = __reduce_add_sync(0xffffffffu, units);
         if (lane == 0 && wsum)
             atomicAdd(reinterpret_cast<unsigned long long *>(ws + 2), (unsigned long long)wsum);
     }
@@ -1084,6 +1336,28 @@ static int persistent_grid(const void *fn, int threads, size_t smem, uint64_t nt
 
 using namespace lu;
 
+template <bool Count>
+static int launch_validate8_lc(const uint8_t *base, uint32_t lead, uint64_t n_units, void *ws, lu_outcome *res,
+                               uint64_t nbytes_frame, cudaStream_t stream)
+{
+    const void *fn = (const void *)k_validate8_lc<Count>;
+    const int sb = (int)kSmemLc;
+    if (int rc = ensure_smem_attr(24 + Count, &fn, &sb, 1))
+        return rc;
+    const uint64_t nsuper = (nbytes_frame + kLcSuper - 1) / kLcSuper;
+    if (nsuper > 0x3fffffffull) // 32-bit slot indices (with head room for sc + slots * warps)
+        return fail(LU_ERR_INVALID, "input too large");
+    const uint64_t nblocks = (nsuper + kWarps - 1) / kWarps;
+    unsigned grid = 0;
+    // at least one CTA: its last warp writes the result (also for empty input)
+    int rc = persistent_grid(fn, kThreads, kSmemLc, nblocks ? nblocks : 1, &grid);
+    if (rc)
+        return rc;
+    k_validate8_lc<Count><<<grid, kThreads, kSmemLc, stream>>>(base, lead, n_units, reinterpret_cast<uint64_t *>(ws),
+                                                               reinterpret_cast<Outcome *>(res), (uint32_t)nsuper);
+    return 0;
+}
+
 template <bool Utf16, bool Count, bool Swap16 = false>
 static int launch_validate(const uint8_t *base, uint32_t lead, uint64_t n_units, void *ws, lu_outcome *res,
                            uint64_t nbytes_frame, cudaStream_t stream)
@@ -1128,6 +1402,9 @@ static int validate_impl(bool utf16, bool count, const uint8_t *inb, uint64_t n_
     else if (utf16)
         rc = count ? launch_validate<true, true>(base, lead, n_units, ws, res, frame, stream)
                    : launch_validate<true, false>(base, lead, n_units, ws, res, frame, stream);
+    else if (LU_K3_LC)
+        rc = count ? launch_validate8_lc<true>(base, lead, n_units, ws, res, frame, stream)
+                   : launch_validate8_lc<false>(base, lead, n_units, ws, res, frame, stream);
     else
         rc = count ? launch_validate<false, true>(base, lead, n_units, ws, res, frame, stream)
                    : launch_validate<false, false>(base, lead, n_units, ws, res, frame, stream);
