@@ -192,14 +192,14 @@ __shared__ unsigned long long s_prof[10][24]; // [warp][counter], lane 0 only
 // malformed.
 constexpr int kScanWarps = 8;
 #ifndef LU_SCAN_PER_LANE
-#define LU_SCAN_PER_LANE 4
+#define LU_SCAN_PER_LANE 3
 #endif
 constexpr int kScanPerLane = LU_SCAN_PER_LANE;
-constexpr uint32_t kScanWindow = 32 * kScanPerLane; // 128 tiles (K1)
-// K2 scans 192-tile windows: its tiles complete faster on latin / cyrillic,
+constexpr uint32_t kScanWindow = 32 * kScanPerLane; // 96 tiles (K1)
+// K2 scans 128-tile windows (re-swept after the early base hand-off; was 192):
 // where the per-window hand-off is the limit
 #ifndef LU_K2_SCAN_PER_LANE
-#define LU_K2_SCAN_PER_LANE 6
+#define LU_K2_SCAN_PER_LANE 4
 #endif
 #ifndef LU_PARTIAL_AFTER
 #define LU_PARTIAL_AFTER 40000
@@ -298,6 +298,26 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
             }
             if (run > done && (partial || run == kWin)) {
                 LU_CNT(11, 1);
+                // Window-local scan first: it does not need the base, so it
+                // runs while the base is still on its way, and the serial
+                // part of the hand-off chain shrinks to wait + add + store.
+                uint32_t lsum = 0, errj = kPL;
+#pragma unroll
+                for (int j = kPL - 1; j >= 0; --j)
+                    if ((uint32_t)j < myr) {
+                        lsum += (uint32_t)s[j]; // aggregate counts are < 2^15
+                        if (s[j] & kErrBit)
+                            errj = (uint32_t)j;
+                    }
+                uint32_t incl = lsum;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= (uint32_t)d)
+                        incl += o;
+                }
+                const uint32_t errball = __ballot_sync(0xffffffffu, errj < kPL);
+                const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
                 if (!have_base) {
                     // Wait for the previous window's base, or for a window
                     // before this one to be known to hold an error.  The
@@ -325,22 +345,16 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                     base = ready == 1 ? vbase[slot] : kErrBit;
                     have_base = true;
                 }
-                uint32_t lsum = 0, errj = kPL;
-#pragma unroll
-                for (int j = kPL - 1; j >= 0; --j)
-                    if ((uint32_t)j < myr) {
-                        lsum += (uint32_t)s[j]; // aggregate counts are < 2^15
-                        if (s[j] & kErrBit)
-                            errj = (uint32_t)j;
-                    }
-                uint32_t incl = lsum;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const uint32_t o = __shfl_up_sync(0xffffffffu, incl, d);
-                    if (lane >= (uint32_t)d)
-                        incl += o;
+                // a complete window hands its end value on before it
+                // publishes its tiles' prefixes (the next window only needs
+                // the base)
+                if (run == kWin && lane == 0) {
+                    if (errball || (base & kErrBit))
+                        atomicMin(&ss.errw, w);
+                    vbase[w % kScanWarps] = (base + wtot) | (errball ? kErrBit : 0ull);
+                    __threadfence_block();
+                    vtag[w % kScanWarps] = w + 1;
                 }
-                const uint32_t errball = __ballot_sync(0xffffffffu, errj < kPL);
                 const bool err_before = (base & kErrBit) || (errball & ((1u << lane) - 1u));
                 uint64_t ex = (base & kValMask) + (incl - lsum);
 #pragma unroll
@@ -352,7 +366,9 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                     ex += (uint32_t)s[j];
                 }
                 done = run;
-                if (errball && run < kWin) {
+                if (run == kWin)
+                    break;
+                if (errball) {
                     // the rest of the window lies behind an error: publish it now
 #pragma unroll
                     for (int j = 0; j < kPL; ++j)
@@ -361,17 +377,6 @@ __device__ __forceinline__ void scan_windows(uint64_t *status, uint32_t ntiles, 
                     if (lane == 0) {
                         atomicMin(&ss.errw, w);
                         vbase[w % kScanWarps] = base | kErrBit;
-                        __threadfence_block();
-                        vtag[w % kScanWarps] = w + 1;
-                    }
-                    break;
-                }
-                if (run == kWin) {
-                    const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
-                    if (lane == 0) {
-                        if (errball || (base & kErrBit))
-                            atomicMin(&ss.errw, w);
-                        vbase[w % kScanWarps] = (base + wtot) | (errball ? kErrBit : 0ull);
                         __threadfence_block();
                         vtag[w % kScanWarps] = w + 1;
                     }

@@ -249,6 +249,7 @@ struct GroupShared {
     uint32_t units[kMaxBufs]; // tile output units before its first error (or all)
     uint32_t claim;
     uint32_t skip; // the claimed tile lies after a tile known to hold an error
+    uint32_t hint_s[kGroupWarps]; // a direction's per-warp hint when it is kept in shared memory (kHintInSmem)
 };
 
 __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n)
@@ -264,7 +265,8 @@ struct DirU8U16T {
     static constexpr int kStride = kOutStrideU16;
     static constexpr int kBufs = kBufsK1;
     static constexpr int kUnitShift = 0; // input positions are bytes
-    static constexpr int kScanPerLane = LU_SCAN_PER_LANE; // 128-tile scanner windows
+    static constexpr int kScanPerLane = LU_SCAN_PER_LANE; // 96-tile scanner windows
+    static constexpr bool kHintInSmem = false;
     using In = ChunkIn;
     template <bool B>
     __device__ static void load(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, uint32_t wit,
@@ -290,7 +292,8 @@ struct DirU16U8T {
     static constexpr int kStride = kOutStrideU8;
     static constexpr int kBufs = kBufsK2;
     static constexpr int kUnitShift = 1; // input positions are 16-bit words
-    static constexpr int kScanPerLane = LU_K2_SCAN_PER_LANE; // 192-tile windows
+    static constexpr int kScanPerLane = LU_K2_SCAN_PER_LANE; // 128-tile windows
+    static constexpr bool kHintInSmem = false;
     using In = ChunkIn;
     template <bool B>
     __device__ static void load(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, uint32_t wit,
@@ -300,9 +303,28 @@ struct DirU16U8T {
     }
     template <bool B>
     __device__ static void compute(const uint8_t *base, int64_t tile_off, int64_t lo_b, int64_t hi_b, OutT *out_w,
-                                   const SelPair *sel, WarpResult &wr, uint32_t wit, const In &in, uint32_t &)
+                                   const SelPair *sel, WarpResult &wr, uint32_t wit, const In &in, uint32_t &hint)
     {
+        // ASCII chunks: a warp whose previous chunk was all ASCII (hint 4)
+        // first tries the narrow-only path.  Kept outside the warp body
+        // (inside it, even out of line, it cost K2 1.5% on every profile).
+        if (LU_K2_ASCII && !B && hint == 4u &&
+            u16u8_ascii_chunk(in.q[0], in.q[1], in.q[2], in.q[3], (uint32_t)__cvta_generic_to_shared(out_w))) {
+            if (lane_id() == 0) {
+                wr.err = 0;
+                wr.pos = 0;
+                wr.units = kChunkBytes / 2;
+            }
+            return;
+        }
         u16u8_warp_r<B>(base, tile_off, lo_b, hi_b, out_w, sel + 16, wr, wit, in);
+        if (LU_K2_ASCII && !B) {
+            // one byte per word and no error: the chunk was all ASCII
+            __syncwarp();
+            const bool ascii = wr.err == 0 && wr.units == (uint32_t)(kChunkBytes / 2);
+            __syncwarp();
+            hint = ascii ? 4u : 2u;
+        }
     }
     __device__ static void copy_out(const OutT *src, uint32_t cnt, OutT *out_a, uint64_t g0)
     {
@@ -542,6 +564,10 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
     const uint32_t gtid = threadIdx.x - g * kGroupThreads;
     const uint32_t bar_claim = 1 + 3 * g, bar_done = 2 + 3 * g, bar_prefix = 3 + 3 * g;
     GroupShared &ps = gshared[g];
+    if (Dir::kHintInSmem) {
+        ps.hint_s[wit] = 2; // every lane writes the same value; only this warp reads it
+        __syncwarp();
+    }
     constexpr uint32_t kBufs = Dir::kBufs;
     OutT *out_g = reinterpret_cast<OutT *>(smem_raw) + g * (kBufs * kGroupWarps * Dir::kStride);
 
@@ -612,10 +638,19 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
         if (tile >= ntiles || skip)
             break;
         OutT *out_w = out_g + (buf * kGroupWarps + wit) * Dir::kStride;
-        if (interior)
-            Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in, hint);
-        else
-            Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in, hint);
+        if constexpr (Dir::kHintInSmem) {
+            if (interior)
+                Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in,
+                                             ps.hint_s[wit]);
+            else
+                Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in,
+                                            ps.hint_s[wit]);
+        } else {
+            if (interior)
+                Dir::template compute<false>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in, hint);
+            else
+                Dir::template compute<true>(base, tile_off, lo_b, hi_b, out_w, sel, ps.wres[buf][wit], wit, in, hint);
+        }
         LU_T(4); // compute
         // poll the status word resolved at the top of the next iteration now:
         // its L2 round trip overlaps the other warps' compute

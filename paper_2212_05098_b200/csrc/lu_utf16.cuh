@@ -125,6 +125,31 @@ __device__ __forceinline__ void sts16b_if(uint32_t addr, uint32_t v, uint32_t n,
                  : "memory");
 }
 
+#ifndef LU_K2_ASCII
+#define LU_K2_ASCII 1
+#endif
+
+// ASCII chunk (every word < 0x80): one vote, then the words' low bytes are
+// packed straight into the staging region (one 8-byte store per round) -- no
+// class votes, no scan, no compaction.  Returns false (nothing stored) if the
+// chunk holds a word >= 0x80.  Out of line so the general body keeps its
+// register allocation (inlined it cost K2 1-2% on every other profile).
+__device__ __noinline__ bool u16u8_ascii_chunk(uint4 q0, uint4 q1, uint4 q2, uint4 q3, uint32_t sbase)
+{
+    const uint32_t lane = lane_id();
+    const uint32_t na = q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w | q2.x | q2.y | q2.z | q2.w | q3.x |
+                        q3.y | q3.z | q3.w;
+    if (__any_sync(0xffffffffu, (na & 0xFF80FF80u) != 0))
+        return false;
+    const uint4 q[4] = {q0, q1, q2, q3};
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(sbase + 256u * r + 8u * lane),
+                     "r"(prmt(q[r].x, q[r].y, 0x6420u)), "r"(prmt(q[r].z, q[r].w, 0x6420u))
+                     : "memory");
+    return true;
+}
+
 // K2 warp body for the pipelined kernel: the warp's 2 KiB chunk (1024 words)
 // in 4 rounds of 512 B, lane l holding words [8l, 8l+8) of the round in
 // registers; neighbour words by shuffle.  Per word: pair-aware UTF-8 encode
@@ -139,6 +164,7 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
     const int64_t chunk = tile_off + (int64_t)warp * kChunkBytes;
     constexpr int kRounds = kChunkBytes / 512;
     const uint4 *q = in.q;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(out_w);
     uint32_t carry = in.halo_p;
     const uint32_t halo_n = in.halo_n;
     uint32_t rn[kRounds];
@@ -146,7 +172,6 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
     for (int r = 0; r < kRounds; ++r)
         rn[r] = __shfl_sync(0xffffffffu, q[r].x, (lane + 1) & 31);
 
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(out_w);
     uint32_t running = 0, err = 0, err_pos = 0, units = 0;
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
@@ -475,6 +500,7 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
     }
     if (!err)
         units = running;
+    // one byte per word: the chunk was all ASCII
     if (lane == 0) {
         wr.err = err;
         wr.pos = err_pos;

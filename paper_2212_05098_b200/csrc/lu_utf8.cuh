@@ -490,6 +490,14 @@ __device__ __forceinline__ void u8_decode3(uint32_t x, uint32_t xn, uint32_t &lo
     hi = hi3 & sA;
 }
 
+// class hint of a warp whose last chunk was all ASCII (hints 0..3 are the class paths)
+constexpr uint32_t kHintAscii = 4;
+
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+{
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
 __device__ __forceinline__ void sts16(uint32_t addr, uint32_t v)
 {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
@@ -726,6 +734,35 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(out_w);
     uint32_t running = 0, err = 0, err_pos = 0, units = 0;
 
+    // ASCII chunks (the paper's ASCII fast path, utf8_to_utf16.py:245-251):
+    // a warp whose previous chunk was all ASCII (kHintAscii) tests the chunk's
+    // bytes with one vote and, if none is >= 0x80, widens them straight into
+    // the staging region with two 16-byte stores per round -- no detector, no
+    // scan, no compaction.
+    if (!Boundary && hint == kHintAscii) {
+        uint32_t na = 0;
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r)
+            na |= q[r].x | q[r].y | q[r].z | q[r].w;
+        if (!__any_sync(0xffffffffu, (na & H8) != 0)) {
+            constexpr uint32_t s01 = BE ? 0x1404u : 0x4140u, s23 = BE ? 0x3424u : 0x4342u;
+#pragma unroll
+            for (int r = 0; r < kRounds; ++r) {
+                const uint32_t a = sbase + 1024u * r + 32u * lane;
+                sts128(a, prmt(q[r].x, 0u, s01), prmt(q[r].x, 0u, s23), prmt(q[r].y, 0u, s01), prmt(q[r].y, 0u, s23));
+                sts128(a + 16, prmt(q[r].z, 0u, s01), prmt(q[r].z, 0u, s23), prmt(q[r].w, 0u, s01),
+                       prmt(q[r].w, 0u, s23));
+            }
+            if (lane == 0) {
+                wr.err = 0;
+                wr.pos = 0;
+                wr.units = kChunkBytes;
+            }
+            return;
+        }
+        hint = 0;
+    }
+
     if (!Boundary && hint < 2) {
         uint32_t miss;
         if (hint == 0)
@@ -733,6 +770,9 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
         else
             miss = u8u16_chunk_fast<1, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
         if (!miss) {
+            // a class-0 chunk that emitted one word per byte is all ASCII
+            if (hint == 0 && running == (uint32_t)kChunkBytes)
+                hint = kHintAscii;
             if (lane == 0) {
                 wr.err = 0;
                 wr.pos = 0;

@@ -87,7 +87,7 @@ def test_device_misalignment(cuda_ok):
             assert out[: got.written].cpu().numpy().tobytes() == ref_payload
 
 
-@pytest.mark.parametrize("profile,seed", [("latin", 1), ("cjk", 3), ("emoji", 4)])
+@pytest.mark.parametrize("profile,seed", [("latin", 1), ("cjk", 3), ("emoji", 4), ("ascii", 7)])
 def test_full_size_be_equals_swapped_le(cuda_ok, profile, seed):
     dev = torch.device("cuda", 0)
     u8 = corpus.generate(profile, 256 << 20, seed, device=dev)

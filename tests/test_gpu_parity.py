@@ -546,6 +546,36 @@ def test_class_switching_text(cuda_ok, utf16):
         check(bytes(b))
 
 
+@pytest.mark.parametrize("utf16", [False, True])
+def test_ascii_chunk_fast_path(cuda_ok, utf16):
+    """Large ASCII buffers run through the persistent pipeline, where a warp
+    whose previous chunk was all ASCII takes the ASCII chunk path (widen /
+    narrow straight into staging).  Pure ASCII, ASCII with isolated multi-unit
+    characters (the warp must leave and re-enter the path), and single errors."""
+    unit = 2 if utf16 else 1
+    n_units = (24 << 20) // unit
+    data = corpus.generate("ascii", n_units, 21, utf16=utf16).numpy().tobytes()
+    assert max(data) < 0x80
+    check = check_u16 if utf16 else check_u8
+    check(data)
+    rng = random.Random(77 + utf16)
+    b = bytearray(data)
+    for _ in range(60):
+        cp = rng.choice([0xE9, 0x416, 0x4E2D, 0xFFFD, 0x1F600, 0x10FFFF])
+        enc = chr(cp).encode("utf-16-le" if utf16 else "utf-8")
+        pos = rng.randrange(0, n_units - 8) * unit
+        b[pos:pos + len(enc)] = enc
+    check(bytes(b))
+    for _ in range(6):
+        e = bytearray(b)
+        pos = rng.randrange(0, n_units) * unit
+        if utf16:
+            e[pos:pos + 2] = rng.choice([0xD800, 0xDC00]).to_bytes(2, "little")
+        else:
+            e[pos] = rng.choice([0x80, 0xC0, 0xE0, 0xF0, 0xFF])
+        check(bytes(e))
+
+
 @pytest.mark.timeout(600)
 def test_error_path_progress_stress(cuda_ok):
     """Repeated transcodes/validations of buffers with errors injected at
