@@ -961,12 +961,12 @@ __global__ void __launch_bounds__(kThreads, LU_LC_CTAS) k_validate8_lc(const uin
     extern __shared__ __align__(128) uint8_t ring[];
     __shared__ __align__(8) uint64_t bar[kWarps * kLcSlots];
     __shared__ WarpResult wr_s[kWarps];
-    __shared__ __align__(8) uint64_t best_s[kWarps];
+    __shared__ __align__(16) uint64_t best_s[2]; // the CTA's copy of the ws header's first 16 bytes
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
     const uint32_t total_warps = gridDim.x * kWarps;
     const uint32_t gw = blockIdx.x * kWarps + warp;
-    const uint32_t best_a = (uint32_t)__cvta_generic_to_shared(&best_s[warp]);
+    const uint32_t best_a = (uint32_t)__cvta_generic_to_shared(&best_s[0]);
     const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n;
     // slots (kLcSub consecutive chunks) whose +-16-byte window lies inside
     // [lo, hi) come through the ring: [1, s_hi) (lead < 16: slot 0 never does)
@@ -981,12 +981,14 @@ __global__ void __launch_bounds__(kThreads, LU_LC_CTAS) k_validate8_lc(const uin
                      "l"(base + (int64_t)sc * kLcSuper - kLcHalo), "r"(kLcSlotBytes), "r"(b)
                      : "memory");
     };
+    if (threadIdx.x == 0)
+        best_s[0] = 0;
     if (lane == 0) {
         for (int k = 0; k < kLcSlots; ++k)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * k));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncwarp();
+    __syncthreads();
     if (lane == 0)
         for (uint32_t k = 0; k < (uint32_t)kLcSlots; ++k) {
             const uint32_t sc = gw + k * total_warps;
@@ -1001,10 +1003,13 @@ __global__ void __launch_bounds__(kThreads, LU_LC_CTAS) k_validate8_lc(const uin
     bool stopped = false;
     for (; sc < nsuper; sc += total_warps) {
         const bool fast = sc >= 1 && sc < s_hi;
-        // published first-error position: fetched now into shared memory
-        // (cp.async: no register held across the chunks), read after them
-        if (lane == 0)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n\tcp.async.commit_group;" ::"r"(best_a), "l"(ws)
+        // Published first-error position: warp 0 of the CTA refreshes a copy in
+        // shared memory every iteration (cp.async: no register held across the
+        // chunks; .cg: through L2 -- an L1-cached copy would never see another
+        // SM's update); every warp reads that copy after its chunks.  One
+        // poller per CTA: every warp polling the same L2 line cost K3 9%.
+        if (warp == 0 && lane == 0)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;" ::"r"(best_a), "l"(ws)
                          : "memory");
         const uint32_t sa0 = ring0 + slot * kLcSlotBytes + kLcHalo;
         if (fast) {
@@ -1064,9 +1069,10 @@ __global__ void __launch_bounds__(kThreads, LU_LC_CTAS) k_validate8_lc(const uin
         // stop once an error is known before this warp's next slot
         uint32_t stop = err;
         if (lane == 0) {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            if (warp == 0)
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
             uint64_t best;
-            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(best) : "r"(best_a) : "memory");
+            asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(best) : "r"(best_a) : "memory");
             if (best != 0)
                 stop |= (uint64_t)(hi_b - (int64_t)best) < (uint64_t)(sc + total_warps) * kLcSuper ? 1u : 0u;
         }
@@ -1420,8 +1426,12 @@ static int validate_impl(bool utf16, bool count, const uint8_t *inb, uint64_t n_
         return fail(LU_ERR_INVALID, "null pointer");
     if ((utf16 && ((uintptr_t)inb & 1)) || ((uintptr_t)ws & 7) || ((uintptr_t)res & 7))
         return fail(LU_ERR_INVALID, "misaligned in/ws/res pointer");
-    if (ws_bytes < 24)
+    // the kernels' 24-byte header starts at the first 16-byte boundary of ws
+    // (k_validate8_lc fetches it with a 16-byte cp.async)
+    const uint64_t ws_skip = (16 - ((uintptr_t)ws & 15)) & 15;
+    if (ws_bytes < 24 + ws_skip)
         return fail(LU_ERR_WORKSPACE, "workspace too small (see lu_workspace_bytes)");
+    ws = reinterpret_cast<uint8_t *>(ws) + ws_skip;
     const uint32_t lead = (uint32_t)((uintptr_t)inb & 15);
     const uint64_t nt = n_tiles(utf16 ? 2 * n_units : n_units, lead);
     if (nt > 0x7fffffffull)

@@ -45,6 +45,8 @@ def short(name: str) -> str:
         return "K1 utf8->utf16 (k_transcode<DirU8U16>)"
     if "DirU16U8" in name or "utf16le_to_utf8" in name:
         return "K2 utf16->utf8"
+    if "k_validate8_lc" in name:
+        return "K3 validate utf8 (k_validate8_lc)"
     if "k_validate" in name:
         # first template flag: Utf16 (k_validate_w<Utf16, Count, Swap16>)
         flags = name.split("<", 1)[1] if "<" in name else ""

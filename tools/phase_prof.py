@@ -31,7 +31,7 @@ def main():
     dev = torch.device("cuda", 0)
     n = 256 << 20
     for utf16 in (False, True):
-        for p, seed in (("latin", 1), ("cyrillic", 2), ("cjk", 3), ("emoji", 4)):
+        for p, seed in (("latin", 1), ("cyrillic", 2), ("cjk", 3), ("emoji", 4), ("ascii", 5)):
             src = corpus.generate(p, n // (2 if utf16 else 1), seed, utf16=utf16, device=dev)
             direction = UTF16_TO_UTF8 if utf16 else UTF8_TO_UTF16
             for _ in range(3):
