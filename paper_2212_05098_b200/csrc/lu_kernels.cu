@@ -8,7 +8,6 @@
 // allocates nothing and keeps no mutable global state (per-call workspace,
 // thread-local error string).
 #include <cstdio>
-#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -263,7 +262,6 @@ __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n)
 template <bool BE>
 struct DirU8U16T {
     using OutT = uint16_t;
-    static constexpr bool kBE = BE;
     static constexpr int kStride = kOutStrideU16;
     static constexpr int kBufs = kBufsK1;
     static constexpr int kUnitShift = 0; // input positions are bytes
@@ -914,10 +912,7 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a)
 // of the chunk's first byte) when the chunk is interior, else masked global
 // loads.  Out of line: it is rare and must not shape the fast path's registers.
 // Returns the new class hint << 32 | this lane's share of the chunk's count.
-// Emit: the count is that of the words EMITTED in the chunk (K1 emits a
-// 4-byte character's low surrogate at its first continuation byte), i.e. an
-// F lead in the chunk's last byte counts in the next chunk.
-template <bool Count, bool Emit = false>
+template <bool Count>
 __device__ __noinline__ uint64_t lc_slow_chunk(const uint8_t *__restrict__ base, int64_t off, int64_t lo_b,
                                                int64_t hi_b, uint32_t sa, bool interior, WarpResult *wr, uint32_t hint)
 {
@@ -934,12 +929,6 @@ __device__ __noinline__ uint64_t lc_slow_chunk(const uint8_t *__restrict__ base,
     } else {
         load_chunk<true>(base, off, lo_b, hi_b, in);
         u8val_warp_in<true, Count>(base, off, lo_b, hi_b, in, *wr, 0, hint, &c);
-    }
-    if (Emit) {
-        if (lane == 0 && in.halo_p >= 0xF0000000u)
-            ++c;
-        if (lane == 31 && in.q[kChunkBytes / 512 - 1].w >= 0xF0000000u && off + kChunkBytes <= hi_b)
-            --c;
     }
     return ((uint64_t)hint << 32) | c;
 }
@@ -964,19 +953,11 @@ __device__ __forceinline__ void lc_load(uint32_t sa, uint32_t lane, uint32_t (&x
     xn = lane == 31 ? hn : xn;
 }
 
-// Emit (stage 1 of the three-stage UTF-8 -> UTF-16 transcode, see k_scatter8):
-// the validator also writes one record per 2 KiB chunk, recs[chunk] = UTF-16
-// words of the chunk | class path << 16 (0, 1, 3, 2 = general, 4 = all ASCII) |
-// error << 31, for every chunk up to the first malformed one.
-constexpr uint32_t kRecErr = 0x80000000u;
-
-template <bool Count, bool Emit = false>
+template <bool Count>
 __global__ void __launch_bounds__(kThreads, LU_LC_CTAS) k_validate8_lc(const uint8_t *__restrict__ base, uint32_t lead,
                                                                        uint64_t n, uint64_t *__restrict__ ws,
-                                                                       Outcome *__restrict__ res, uint32_t nsuper,
-                                                                       uint32_t *__restrict__ recs = nullptr)
+                                                                       Outcome *__restrict__ res, uint32_t nsuper)
 {
-    static_assert(Count || !Emit, "chunk records carry the chunk's count");
     extern __shared__ __align__(128) uint8_t ring[];
     __shared__ __align__(8) uint64_t bar[kWarps * kLcSlots];
     __shared__ WarpResult wr_s[kWarps];
@@ -1063,26 +1044,11 @@ __global__ void __launch_bounds__(kThreads, LU_LC_CTAS) k_validate8_lc(const uin
                     slow = __any_sync(0xffffffffu, fd != 0);
                 }
                 // 64 bytes per lane minus continuations plus 4-byte leads
-                uint32_t mine = 64u - (c_nc >> 7) + (c_nf >> 7);
-                if (Emit) {
-                    // words emitted IN this chunk: a 4-byte character's low
-                    // surrogate is emitted at its first continuation byte
-                    if (lane == 0 && xp >= 0xF0000000u)
-                        ++mine;
-                    if (lane == 31 && x[kLcQuads - 1] >= 0xF0000000u)
-                        --mine;
-                }
                 if (Count && !slow)
-                    units += mine;
-                if (Emit && !slow) {
-                    const uint32_t tot = __reduce_add_sync(0xffffffffu, mine);
-                    if (lane == 0)
-                        recs[off / kChunkBytes] =
-                            tot | ((hint == 0 && tot == (uint32_t)kChunkBytes) ? 4u : hint) << 16;
-                }
+                    units += 64u - (c_nc >> 7) + (c_nf >> 7);
             }
             if (slow) {
-                const uint64_t hc = lc_slow_chunk<Count, Emit>(base, off, lo_b, hi_b, sa, fast, &wr_s[warp], hint);
+                const uint64_t hc = lc_slow_chunk<Count>(base, off, lo_b, hi_b, sa, fast, &wr_s[warp], hint);
                 hint = (uint32_t)(hc >> 32);
                 __syncwarp();
                 err = wr_s[warp].err;
@@ -1090,12 +1056,6 @@ __global__ void __launch_bounds__(kThreads, LU_LC_CTAS) k_validate8_lc(const uin
                 __syncwarp();
                 if (Count)
                     units += (uint32_t)hc; // this lane's share of the chunk's count (u8val_warp_in)
-                if (Emit) {
-                    // general class: the scatter stage decodes such chunks with the general decoder
-                    const uint32_t tot = __reduce_add_sync(0xffffffffu, (uint32_t)hc);
-                    if (lane == 0)
-                        recs[off / kChunkBytes] = tot | 2u << 16 | (err ? kRecErr : 0u);
-                }
                 if (err) {
                     if (lane == 0) {
                         const uint64_t pu = (uint64_t)(off + pos - lo_b);
@@ -1155,331 +1115,6 @@ __global__ void __launch_bounds__(kThreads, LU_LC_CTAS) k_validate8_lc(const uin
             res->consumed = n - b;
             res->written = (Count && !b) ? atomicAdd(reinterpret_cast<unsigned long long *>(ws + 2), 0ull) : 0;
         }
-    }
-}
-
-// ======================================= three-stage UTF-8 -> UTF-16 (K1-3S)
-//
-// north_star's three stages as three stream-ordered launches, for inputs large
-// enough that two more launches do not matter:
-//   1. k_validate8_lc<true, true>: validate, first error position, and one
-//      record per 2 KiB chunk (UTF-16 words emitted in the chunk, class path);
-//   2. k_scan_chunks: exclusive scan of the chunk counts (4096 chunks per CTA,
-//      the last CTA to finish scans the block totals);
-//   3. k_scatter8: decode + compact + store.  Every warp knows its chunk's
-//      output offset before it starts, so there is no ordering protocol at
-//      all (no tickets, no scanner, no group barriers, no deferred copy-out):
-//      warp g takes chunks g, g + G, ... through a private TMA ring, decodes
-//      with the chunk's class decoder (no detector: stage 1 validated it),
-//      compacts into a staging region written at the output's 16-byte phase,
-//      and copies out with aligned 16-byte loads and stores (no shifts).
-// The input is read twice (stage 3 mostly from HBM again); the single-pass
-// pipeline (k_transcode) stays for small inputs and as the fallback when the
-// caller's workspace is too small for the chunk records.
-// ws (16-byte aligned): [64 B header as k_validate_w, + u32 scan CTAs done at
-// byte 24][recs u32 x nchunks][lpre u32 x nchunks][bpre u64 x (nblocks + 1)].
-
-constexpr int kScanThreads = 1024;
-constexpr int kScanPerCta = 4 * kScanThreads; // chunks per scan CTA
-
-struct K1Ws {
-    uint64_t *hdr;
-    uint32_t *recs;
-    uint32_t *lpre;
-    uint64_t *bpre;
-};
-
-__host__ __device__ inline uint64_t k1ws_bytes(uint64_t nchunks)
-{
-    const uint64_t nc4 = (nchunks + 3) & ~3ull;
-    const uint64_t nb = (nchunks + kScanPerCta - 1) / kScanPerCta;
-    return 64 + 4 * nc4 + 4 * nc4 + 8 * (nb + 2);
-}
-
-__host__ __device__ inline K1Ws k1ws_layout(void *ws16, uint64_t nchunks)
-{
-    const uint64_t nc4 = (nchunks + 3) & ~3ull;
-    K1Ws w;
-    uint8_t *p = reinterpret_cast<uint8_t *>(ws16);
-    w.hdr = reinterpret_cast<uint64_t *>(p);
-    w.recs = reinterpret_cast<uint32_t *>(p + 64);
-    w.lpre = reinterpret_cast<uint32_t *>(p + 64 + 4 * nc4);
-    w.bpre = reinterpret_cast<uint64_t *>(p + 64 + 8 * nc4);
-    return w;
-}
-
-// first chunk that is not scanned / scattered normally: the chunk holding the
-// first error (everything after it is ignored), or nchunks
-__device__ __forceinline__ uint32_t k1_limit(const uint64_t *hdr, uint32_t lead, uint64_t n, uint32_t nchunks)
-{
-    const uint64_t best = hdr[0];
-    return best ? (uint32_t)((lead + (n - best)) / kChunkBytes) : nchunks;
-}
-
-__global__ void __launch_bounds__(kScanThreads) k_scan_chunks(K1Ws w, uint32_t lead, uint64_t n, uint32_t nchunks)
-{
-    __shared__ uint32_t wsum[kScanThreads / 32];
-    __shared__ uint32_t last_s;
-    const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const uint32_t limit = k1_limit(w.hdr, lead, n, nchunks);
-    const uint32_t c0 = blockIdx.x * kScanPerCta + 4 * t;
-    uint4 r = make_uint4(0, 0, 0, 0);
-    if (c0 < limit) // (recs is padded to a multiple of 4; entries >= limit are masked below)
-        r = *reinterpret_cast<const uint4 *>(w.recs + c0);
-    const uint32_t v0 = c0 < limit ? (r.x & 0xFFFFu) : 0u, v1 = c0 + 1 < limit ? (r.y & 0xFFFFu) : 0u,
-                   v2 = c0 + 2 < limit ? (r.z & 0xFFFFu) : 0u, v3 = c0 + 3 < limit ? (r.w & 0xFFFFu) : 0u;
-    const uint32_t mine = v0 + v1 + v2 + v3;
-    const uint32_t incl = warp_incl_scan(mine);
-    if (lane == 31)
-        wsum[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t x = wsum[lane];
-        const uint32_t xi = warp_incl_scan(x);
-        wsum[lane] = xi - x;
-        if (lane == 31)
-            w.bpre[1 + blockIdx.x] = xi; // block total; turned into a prefix below
-    }
-    __syncthreads();
-    const uint32_t ex = wsum[warp] + incl - mine;
-    if (c0 <= limit && c0 < nchunks) // (<=: the error chunk's own offset is needed too)
-        *reinterpret_cast<uint4 *>(w.lpre + c0) = make_uint4(ex, ex + v0, ex + v0 + v1, ex + v0 + v1 + v2);
-    // the last CTA to finish turns the block totals into exclusive prefixes
-    __threadfence();
-    __syncthreads();
-    if (t == 0)
-        last_s = atomicAdd(reinterpret_cast<unsigned int *>(w.hdr + 3), 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last_s)
-        return;
-    __threadfence();
-    if (warp == 0) {
-        uint64_t carry = 0;
-        for (uint32_t b0 = 0; b0 < gridDim.x; b0 += 32) {
-            const uint32_t b = b0 + lane;
-            const uint64_t x = b < gridDim.x ? *reinterpret_cast<volatile uint64_t *>(w.bpre + 1 + b) : 0ull;
-            uint64_t xi = x;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint64_t o = __shfl_up_sync(0xffffffffu, xi, d);
-                if (lane >= (uint32_t)d)
-                    xi += o;
-            }
-            if (b < gridDim.x)
-                w.bpre[1 + b] = carry + xi; // inclusive: bpre[b + 1] = prefix of block b + 1
-            carry += __shfl_sync(0xffffffffu, xi, 31);
-        }
-        if (lane == 0)
-            w.bpre[0] = 0;
-    }
-}
-
-// copy cnt words staged at src[shift ..] (src 16-byte aligned, shift = g0 & 7:
-// the staging region has the output's 16-byte phase) to out_a[g0 ..)
-__device__ __forceinline__ void copy_out_u16_aligned(const uint16_t *src, uint32_t shift, uint32_t cnt,
-                                                     uint16_t *out_a, uint64_t g0)
-{
-    if (cnt == 0)
-        return;
-    const uint32_t lane = lane_id();
-    uint16_t *dst = out_a + (g0 - shift); // 16-byte aligned
-    const uint32_t total = shift + cnt;
-    const uint32_t full_lo = shift ? 1u : 0u, full_hi = total >> 3;
-    const uint4 *s128 = reinterpret_cast<const uint4 *>(src);
-    uint4 *d128 = reinterpret_cast<uint4 *>(dst);
-#pragma unroll 2
-    for (uint32_t c = full_lo + lane; c < full_hi; c += 32)
-        __stcs(d128 + c, s128[c]);
-    if (lane < 16) {
-        uint32_t chunk;
-        if (lane < 8)
-            chunk = shift ? 0u : 0xffffffffu;
-        else
-            chunk = (total & 7) && !(shift && full_hi == 0) ? full_hi : 0xffffffffu;
-        if (chunk != 0xffffffffu) {
-            const uint32_t i = 8 * chunk + (lane & 7);
-            if (i >= shift && i < total)
-                dst[i] = src[i];
-        }
-    }
-}
-
-// One valid chunk of class P: four rounds of mask fill + u8u16_round<P> (decode,
-// scan, compaction into the staging region at word offset `shift`).  Returns
-// the number of words staged.
-template <int P, bool BE>
-__device__ __forceinline__ uint32_t scatter_chunk(const ChunkIn &in, const uint8_t *__restrict__ base, int64_t off,
-                                                  int64_t lo_b, int64_t hi_b, uint32_t sbase, const SelPair *sel,
-                                                  uint32_t shift)
-{
-    const uint32_t lane = lane_id();
-    constexpr int kRounds = kChunkBytes / 512;
-    const uint4 *q = in.q;
-    uint32_t rn[kRounds];
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r)
-        rn[r] = __shfl_sync(0xffffffffu, q[r].x, (lane + 1) & 31);
-    uint32_t carry = in.halo_p;
-    uint32_t running = shift, err = 0, err_pos = 0, units = 0;
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
-        const int64_t lane_off = off + r * 512 + 16 * (int64_t)lane;
-        const uint32_t rp = __shfl_sync(0xffffffffu, q[r].w, (lane + 31) & 31);
-        U8Round R;
-        R.w[0] = (lane == 0) ? carry : rp;
-        carry = rp;
-        R.w[1] = q[r].x;
-        R.w[2] = q[r].y;
-        R.w[3] = q[r].z;
-        R.w[4] = q[r].w;
-        R.w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : in.halo_n) : rn[r];
-#pragma unroll
-        for (int k = 0; k <= 4; ++k) {
-            const uint32_t x = R.w[k];
-            if (P == 2) {
-                R.m[k] = u8_classify(x);
-            } else {
-                const uint32_t t1 = x << 1;
-                R.m[k].C = x & ~t1 & H8;
-                R.m[k].L = 0;
-                R.m[k].E = 0;
-                R.m[k].F = P == 3 ? (x & t1 & (x << 2) & (x << 3) & H8) : 0u;
-                if (P == 3 && k >= 1)
-                    R.key[k] = ((x & 0x07070707u) << 2) | ((fsr(x, R.w[k + 1], 8) >> 4) & 0x03030303u);
-            }
-        }
-        R.path = P;
-        R.det = 0;
-        u8u16_round<P, false, BE>(R, r, base, off, off, lane_off, lo_b, hi_b, sbase, sel, running, err, err_pos,
-                                  units);
-    }
-    return running - shift;
-}
-
-// Chunks the straight path does not take: the chunk holding the first error,
-// the first / last chunks of the input (their window leaves [lo, hi)), and
-// all-ASCII chunks (widened into the staging region at phase 0).  The
-// round-layout warp body of the single-pass kernel stages the chunk (exact
-// error position, units before it), copy_out_u16 shifts it into place.
-template <bool BE>
-__device__ __noinline__ uint32_t scatter_slow_chunk(const uint8_t *__restrict__ base, int64_t off, int64_t lo_b,
-                                                    int64_t hi_b, uint32_t sa, bool interior, uint32_t ascii,
-                                                    uint16_t *stage, const SelPair *sel, WarpResult *wr,
-                                                    uint16_t *out_a, uint64_t g0)
-{
-    const uint32_t lane = lane_id();
-    ChunkIn in;
-    uint32_t hint = ascii ? kHintAscii : 2u;
-    if (interior) {
-#pragma unroll
-        for (int r = 0; r < kChunkBytes / 512; ++r)
-            in.q[r] = lds128(sa + r * 512 + 16 * lane);
-        in.halo_p = lds32(sa - 4);
-        in.halo_n = lds32(sa + kChunkBytes);
-        u8u16_warp<false, BE>(base, off, lo_b, hi_b, stage, sel, *wr, 0, in, hint);
-    } else {
-        load_chunk<true>(base, off, lo_b, hi_b, in);
-        u8u16_warp<true, BE>(base, off, lo_b, hi_b, stage, sel, *wr, 0, in, hint);
-    }
-    __syncwarp();
-    const uint32_t units = wr->units;
-    copy_out_u16(stage, units, out_a, g0);
-    __syncwarp();
-    return units;
-}
-
-constexpr int kScSlots = 2;
-constexpr int kScSlotBytes = kChunkBytes + 2 * kLcHalo;
-constexpr size_t kSmemScatter = (size_t)kWarps * (kScSlots * kScSlotBytes + sizeof(uint16_t) * kOutStrideU16);
-
-template <bool BE>
-__global__ void __launch_bounds__(kThreads, 3) k_scatter8(const uint8_t *__restrict__ base, uint32_t lead, uint64_t n,
-                                                          uint16_t *__restrict__ out_a, uint32_t out_lead, K1Ws w,
-                                                          Outcome *__restrict__ res, uint32_t nchunks)
-{
-    extern __shared__ __align__(128) uint8_t smem_sc[];
-    __shared__ __align__(8) uint64_t bar[kWarps * kScSlots];
-    __shared__ SelPair sel[40];
-    __shared__ WarpResult wr_s[kWarps];
-    const uint32_t warp = threadIdx.x >> 5;
-    const uint32_t lane = lane_id();
-    const uint32_t total_warps = gridDim.x * kWarps;
-    const uint32_t gw = blockIdx.x * kWarps + warp;
-    const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)n;
-    const uint32_t limit = k1_limit(w.hdr, lead, n, nchunks); // chunks [0, limit] are processed
-    const uint32_t last = limit < nchunks ? limit : nchunks - 1;
-    // interior chunks (their +-16-byte window lies inside [lo, hi)) come through the ring
-    const uint32_t c_hi = hi_b >= kChunkBytes + kLcHalo ? (uint32_t)((hi_b - kLcHalo) / kChunkBytes) : 0u;
-    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bar[warp * kScSlots]);
-    uint8_t *my = smem_sc + warp * (kScSlots * kScSlotBytes + sizeof(uint16_t) * kOutStrideU16);
-    const uint32_t ring0 = (uint32_t)__cvta_generic_to_shared(my);
-    uint16_t *stage = reinterpret_cast<uint16_t *>(my + kScSlots * kScSlotBytes);
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(stage);
-    auto issue = [&](uint32_t c, uint32_t slot) {
-        const uint32_t b = bar0 + 8 * slot;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kScSlotBytes) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         ring0 + slot * kScSlotBytes),
-                     "l"(base + (int64_t)c * kChunkBytes - kLcHalo), "r"(kScSlotBytes), "r"(b)
-                     : "memory");
-    };
-    sel_table_init(sel);
-    if (lane == 0) {
-        for (int k = 0; k < kScSlots; ++k)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * k));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (lane == 0)
-        for (uint32_t k = 0; k < (uint32_t)kScSlots; ++k) {
-            const uint32_t c = gw + k * total_warps;
-            if (c <= last && c >= 1 && c < c_hi)
-                issue(c, k);
-        }
-    uint32_t parity = 0, slot = 0;
-    for (uint32_t c = gw; c <= last; c += total_warps) {
-        const bool fast = c >= 1 && c < c_hi;
-        const int64_t off = (int64_t)c * kChunkBytes;
-        const uint32_t rec = w.recs[c];
-        const uint64_t g0 = (uint64_t)out_lead + w.bpre[c / kScanPerCta] + w.lpre[c];
-        const uint32_t sa = ring0 + slot * kScSlotBytes + kLcHalo;
-        if (fast) {
-            mbar_wait(bar0 + 8 * slot, (parity >> slot) & 1);
-            parity ^= 1u << slot;
-        }
-        const uint32_t cls = (rec >> 16) & 7u;
-        if (!fast || (rec & kRecErr) || cls == 4u) {
-            const uint32_t units =
-                scatter_slow_chunk<BE>(base, off, lo_b, hi_b, sa, fast, cls == 4u, stage, sel, &wr_s[warp], out_a, g0);
-            if ((rec & kRecErr) && lane == 0)
-                res->written = g0 - out_lead + units; // stage 1 wrote status and consumed
-        } else {
-            ChunkIn in;
-#pragma unroll
-            for (int r = 0; r < kChunkBytes / 512; ++r)
-                in.q[r] = lds128(sa + r * 512 + 16 * lane);
-            in.halo_p = lds32(sa - 4);
-            in.halo_n = lds32(sa + kChunkBytes);
-            const uint32_t shift = (uint32_t)g0 & 7u;
-            uint32_t cnt;
-            if (cls == 0)
-                cnt = scatter_chunk<0, BE>(in, base, off, lo_b, hi_b, sbase, sel, shift);
-            else if (cls == 1)
-                cnt = scatter_chunk<1, BE>(in, base, off, lo_b, hi_b, sbase, sel, shift);
-            else if (cls == 3)
-                cnt = scatter_chunk<3, BE>(in, base, off, lo_b, hi_b, sbase, sel, shift);
-            else
-                cnt = scatter_chunk<2, BE>(in, base, off, lo_b, hi_b, sbase, sel, shift);
-            __syncwarp();
-            copy_out_u16_aligned(stage, shift, cnt, out_a, g0);
-        }
-        __syncwarp(); // every lane is done with the slot and the staging region
-        if (lane == 0) {
-            const uint32_t cn = c + kScSlots * total_warps;
-            if (cn <= last && cn >= 1 && cn < c_hi)
-                issue(cn, slot);
-        }
-        slot = slot == kScSlots - 1 ? 0u : slot + 1;
     }
 }
 
@@ -1860,71 +1495,6 @@ static int chars_impl(bool utf16, const uint8_t *inb, uint64_t n_units, void *ws
     return 0;
 }
 
-#ifndef LU_K1_3S
-#define LU_K1_3S 1 // large UTF-8 -> UTF-16 inputs through the three-stage kernels
-#endif
-#ifndef LU_K1_3S_MIN
-#define LU_K1_3S_MIN (32ull << 20) // bytes; below it the two extra launches are not worth it
-#endif
-
-// LU_K1_3S_MIN_BYTES in the environment overrides the threshold (tests run the
-// whole parity suite through the three-stage kernels with it set to 1)
-static uint64_t k1_3s_min()
-{
-    static const uint64_t v = [] {
-        const char *e = getenv("LU_K1_3S_MIN_BYTES");
-        return e && *e ? (uint64_t)strtoull(e, nullptr, 10) : (uint64_t)LU_K1_3S_MIN;
-    }();
-    return v;
-}
-
-static uint64_t k1_3s_ws_bytes(uint64_t n_bytes)
-{
-    return 16 + k1ws_bytes((n_bytes + 15 + kChunkBytes - 1) / kChunkBytes);
-}
-
-// Three-stage UTF-8 -> UTF-16 (k_validate8_lc<true, true> -> k_scan_chunks -> k_scatter8)
-template <bool BE>
-static int u8u16_3s_launch(const uint8_t *base, uint32_t lead, uint64_t n_bytes, uint16_t *out_a, uint32_t out_lead,
-                           void *ws, lu_outcome *res, cudaStream_t stream)
-{
-    const uint64_t frame = lead + n_bytes;
-    const uint64_t nchunks = (frame + kChunkBytes - 1) / kChunkBytes;
-    if (nchunks > 0x3fffffffull)
-        return fail(LU_ERR_INVALID, "input too large");
-    void *ws16 = reinterpret_cast<void *>(((uintptr_t)ws + 15) & ~(uintptr_t)15);
-    const K1Ws w = k1ws_layout(ws16, nchunks);
-    cudaError_t e = cudaMemsetAsync(ws16, 0, 64, stream);
-    if (e != cudaSuccess)
-        return cuda_fail(e, "cudaMemsetAsync");
-    const void *fa = (const void *)k_validate8_lc<true, true>;
-    const void *fc = (const void *)k_scatter8<BE>;
-    const int sa = (int)kSmemLc, sc = (int)kSmemScatter;
-    if (int rc = ensure_smem_attr(26, &fa, &sa, 1))
-        return rc;
-    if (int rc = ensure_smem_attr(27 + BE, &fc, &sc, 1))
-        return rc;
-    unsigned grid = 0;
-    const uint64_t nsuper = (frame + kLcSuper - 1) / kLcSuper;
-    int rc = persistent_grid(fa, kThreads, kSmemLc, (nsuper + kWarps - 1) / kWarps, &grid);
-    if (rc)
-        return rc;
-    k_validate8_lc<true, true><<<grid, kThreads, kSmemLc, stream>>>(base, lead, n_bytes, w.hdr,
-                                                                     reinterpret_cast<Outcome *>(res),
-                                                                     (uint32_t)nsuper, w.recs);
-    const unsigned nb = (unsigned)((nchunks + kScanPerCta - 1) / kScanPerCta);
-    k_scan_chunks<<<nb, kScanThreads, 0, stream>>>(w, lead, n_bytes, (uint32_t)nchunks);
-    rc = persistent_grid(fc, kThreads, kSmemScatter, (nchunks + kWarps - 1) / kWarps, &grid);
-    if (rc)
-        return rc;
-    k_scatter8<BE><<<grid, kThreads, kSmemScatter, stream>>>(base, lead, n_bytes, out_a, out_lead, w,
-                                                             reinterpret_cast<Outcome *>(res), (uint32_t)nchunks);
-    e = cudaGetLastError();
-    if (e != cudaSuccess)
-        return cuda_fail(e, "three-stage utf8_to_utf16 launch");
-    return 0;
-}
-
 template <class Dir>
 static int u8u16_impl(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint64_t out_cap_words, void *ws,
                       uint64_t ws_bytes, lu_outcome *res, cudaStream_t stream)
@@ -1943,10 +1513,6 @@ static int u8u16_impl(const uint8_t *in, uint64_t n_bytes, uint16_t *out, uint64
         return fail(LU_ERR_WORKSPACE, "workspace too small (see lu_workspace_bytes)");
     if (nt > 0x7fffffffull)
         return fail(LU_ERR_INVALID, "input too large");
-    if (LU_K1_3S && n_bytes > 0 && n_bytes >= k1_3s_min() && ws_bytes >= k1_3s_ws_bytes(n_bytes)) {
-        const uint32_t ol = (uint32_t)(((uintptr_t)out & 15) >> 1);
-        return u8u16_3s_launch<Dir::kBE>(in - lead, lead, n_bytes, out - ol, ol, ws, res, stream);
-    }
     int rc = set_smem_attrs();
     if (rc)
         return rc;
@@ -2086,13 +1652,8 @@ uint64_t lu_workspace_bytes(int op, uint64_t n_units)
 {
     switch (op) {
     case LU_OP_UTF8_TO_UTF16LE:
-    case LU_OP_UTF8_TO_UTF16BE: {
-        // single-pass pipeline: a status word per 8 KiB tile; three-stage
-        // kernels (large inputs): 8 bytes per 2 KiB chunk
-        const uint64_t a = 8 * (n_tiles(n_units, 15, kPipeTile) + 2) + 64;
-        const uint64_t b = (LU_K1_3S && n_units >= k1_3s_min()) ? k1_3s_ws_bytes(n_units) : 0;
-        return a > b ? a : b;
-    }
+    case LU_OP_UTF8_TO_UTF16BE:
+        return 8 * (n_tiles(n_units, 15, kPipeTile) + 2) + 64;
     case LU_OP_UTF16LE_TO_UTF8:
     case LU_OP_UTF16BE_TO_UTF8:
         return 8 * (n_tiles(2 * n_units, 15, kPipeTile) + 2) + 64;

@@ -136,9 +136,7 @@ __device__ __forceinline__ uint32_t lc_detect_general(const uint32_t (&x)[kLcQua
                                                       uint32_t &nc, uint32_t &nf, uint32_t &cls)
 {
     U8Masks p = u8_classify(xp), c = p;
-    // the look-behind quad's leads count towards the class: their sequences
-    // may end in this chunk (a decoder of a narrower class would miss them)
-    uint32_t det = 0, o2 = p.L & ~p.E, o3 = p.E & ~p.F, o4 = p.F;
+    uint32_t det = 0, o2 = 0, o3 = 0, o4 = 0;
 #pragma unroll
     for (int k = 0; k < kLcQuads; ++k) {
         const uint32_t v = x[k];
