@@ -537,6 +537,7 @@ __device__ __forceinline__ void u16val_warp_in(int64_t tile_off, int64_t lo_b, i
         hcarry = hsh;
     }
     uint32_t cnt = 0;
+    uint32_t accp = 0, accl = 0; // Count, interior chunks: 128 x (class hits), 128 x (low surrogates), by dp4a
     err = 0;
     err_pos = 0;
 #pragma unroll
@@ -574,7 +575,16 @@ __device__ __forceinline__ void u16val_warp_in(int64_t tile_off, int64_t lo_b, i
                 }
                 const uint32_t hs = ~(g ? hsB : hsA) & H8, ls = (g ? lsB : lsA) & H8;
                 // out-of-range words read as 0: no big/mid/surrogate bits
-                cnt += __popc(one) + __popc(big) + __popc(mid) + __popc(hs) - 3 * __popc(ls);
+                if (Boundary) {
+                    cnt += __popc(one) + __popc(big) + __popc(mid) + __popc(hs) - 3 * __popc(ls);
+                } else {
+                    // interior: every word counts 1 (added at the end); the class
+                    // bits are summed by dp4a (one multiply-add each, no POPC)
+                    accp = __dp4a(big, 0x01010101u, accp);
+                    accp = __dp4a(mid, 0x01010101u, accp);
+                    accp = __dp4a(hs, 0x01010101u, accp);
+                    accl = __dp4a(ls, 0x01010101u, accl);
+                }
             }
         }
         if (__any_sync(0xffffffffu, det != 0)) {
@@ -623,7 +633,7 @@ __device__ __forceinline__ void u16val_warp_in(int64_t tile_off, int64_t lo_b, i
         }
     }
     if (Count)
-        *count = cnt;
+        *count = Boundary ? cnt : (uint32_t)(kChunkBytes / 64) + (accp >> 7) - 3 * (accl >> 7);
 }
 
 template <bool Boundary, bool Count = false, bool Swap16 = false>
