@@ -138,7 +138,7 @@ struct WarpResult {
 struct U8Round {
     uint32_t w[6];   // xp, q0..q3, xn
     U8Masks m[5];    // masks of w[0..4] (F only computed off path 0)
-    uint32_t key[5]; // path 3 (fast): per byte (lead & 7) << 2 | (next >> 4) & 3 (u8_check_f), quads 1..4
+    uint32_t key[5]; // path 3 (fast): per byte plane - 1 of a 4-byte lead (u8_plane_m1), quads 1..4
     uint32_t det;    // nonzero: a bad byte may lie in this lane's 16 bytes
     int path;
 };
@@ -149,11 +149,20 @@ __device__ __forceinline__ uint32_t u8_check_e(uint32_t x, uint32_t n1, const U8
     const uint32_t u = ((x & 0x0F0F0F0Fu) << 1) | ((n1 >> 5) & 0x01010101u);
     return c.E & ~c.F & ~((u + 0x7F7F7F7Fu) & ((u ^ 0x1B1B1B1Bu) + 0x7F7F7F7Fu));
 }
+// Per byte (a 4-byte lead x with second byte n1): plane - 1 in bits 0..4,
+// where plane = (x & 7) << 2 | (n1 >> 4) & 3 is the code point >> 16.  Valid
+// planes are 1..16, so bit 4 is set exactly for plane 0 (F0 80..8F, overlong)
+// and planes 17..31 (F4 90.. / F5..F7, > U+10FFFF); bit 5 keeps the
+// subtraction from borrowing across bytes.  The path-3 decoder reuses the
+// value (high surrogate = D800 | (plane - 1) << 6 | ...).
+__device__ __forceinline__ uint32_t u8_plane_m1(uint32_t x, uint32_t n1)
+{
+    return (((x & 0x07070707u) << 2) | ((n1 >> 4) & 0x03030303u) | 0x20202020u) - 0x01010101u;
+}
 // F0 80..8F (overlong), F4 90.. / F5..F7 (> U+10FFFF), F8..FF
 __device__ __forceinline__ uint32_t u8_check_f(uint32_t x, uint32_t n1, const U8Masks &c)
 {
-    const uint32_t key = ((x & 0x07070707u) << 2) | ((n1 >> 4) & 0x03030303u);
-    return c.F & (~(key + 0x7F7F7F7Fu) | (key + 0x6F6F6F6Fu) | (x << 4));
+    return c.F & ((u8_plane_m1(x, n1) << 3) | (x << 4));
 }
 // E-class bytes whose low nibble is 0, D, E or F (E0 / ED candidates)
 __device__ __forceinline__ uint32_t u8_prefilter_e(uint32_t x, const U8Masks &c)
@@ -362,9 +371,9 @@ __device__ __forceinline__ uint32_t u8_fast3(U8Round &R)
         spill = __umulhi(F, 0x01010100u);
         det |= need ^ C;
         det |= L & ~F;                                     // a 2- or 3-byte lead: not this class
-        // F0 80..8F, F4 90.., F5..FF (u8_check_f); the key is kept for the decoder
-        const uint32_t key = ((x & 0x07070707u) << 2) | ((fsr(x, R.w[k + 1], 8) >> 4) & 0x03030303u);
-        det |= F & (~(key + 0x7F7F7F7Fu) | (key + 0x6F6F6F6Fu) | (x << 4));
+        // F0 80..8F, F4 90.., F5..FF (u8_check_f); plane - 1 is kept for the decoder
+        const uint32_t key = u8_plane_m1(x, fsr(x, R.w[k + 1], 8));
+        det |= F & ((key << 3) | (x << 4));
         R.key[k] = key;
         R.m[k].C = C;
         R.m[k].L = F;
@@ -457,9 +466,9 @@ __device__ __forceinline__ void u8_decode4(uint32_t x, uint32_t xn, const U8Mask
     // low surrogate at the first continuation: DC00 | (b1 & 0xF) << 6 | b2 & 0x3F
     const uint32_t lo3 = ((n1 << 6) & 0xC0C0C0C0u) | (n2 & 0x3F3F3F3Fu);
     const uint32_t hiS = 0xDCDCDCDCu | ((n1 >> 2) & 0x03030303u);
-    // high surrogate at the lead: (cp >> 10) - 0x40 = (key - 1) << 6 | (b1 & 0xF) << 2 | b2 >> 4 & 3,
-    // key = (b0 & 7) << 2 | b1 >> 4 & 3 >= 1 for valid leads (computed by the detector)
-    const uint32_t km1 = (key | H8) - 0x01010101u; // per byte, no borrow across bytes
+    // high surrogate at the lead: (cp >> 10) - 0x40 = (plane - 1) << 6 | (b1 & 0xF) << 2 | b2 >> 4 & 3;
+    // key = plane - 1 in bits 0..4 (u8_plane_m1, computed by the detector)
+    const uint32_t km1 = key;
     const uint32_t hi4 = ((km1 >> 2) & 0x07070707u) | 0xD8D8D8D8u;
     const uint32_t lo4 = ((km1 << 6) & 0xC0C0C0C0u) | ((n1 << 2) & 0x3C3C3C3Cu) | ((n2 >> 4) & 0x03030303u);
     const uint32_t sA = sgn8(x);

@@ -116,8 +116,7 @@ __device__ __forceinline__ uint32_t lc_detect(const uint32_t (&x)[kLcQuads], uin
             spill = __umulhi(F, 0x01010100u);
             det |= need ^ C;
             det |= L & ~F; // a 2- or 3-byte lead: not this class
-            const uint32_t key = ((v & 0x07070707u) << 2) | ((fsr(v, vn, 8) >> 4) & 0x03030303u);
-            det |= F & (~(key + 0x7F7F7F7Fu) | (key + 0x6F6F6F6Fu) | (v << 4));
+            det |= F & ((u8_plane_m1(v, fsr(v, vn, 8)) << 3) | (v << 4));
             if (Count) {
                 nc = __dp4a(C, 0x01010101u, nc);
                 nf = __dp4a(F, 0x01010101u, nf);
