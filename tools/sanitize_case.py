@@ -30,6 +30,14 @@ for profile in ("latin", "emoji", "mix"):
         lu.validate_device(lu.UTF16_TO_UTF8, s)
         lu.count_device(lu._native.OP_UTF8_LENGTH_FROM_UTF16LE, s)
         lu.count_device(lu._native.OP_UTF16LE_CHAR_COUNT, s)
+# persistent pipeline + ASCII chunk paths (needs more tiles than resident groups)
+if len(sys.argv) > 1 and sys.argv[1] == "ascii":
+    a8 = corpus.generate("ascii", 10 << 20, 9, device=dev)
+    a8[5_000_001] = 0xC3
+    a8[5_000_002] = 0xA9
+    lu.transcode_device(lu.UTF8_TO_UTF16, a8)
+    a16 = corpus.generate("ascii", 5 << 20, 9, utf16=True, device=dev)
+    lu.transcode_device(lu.UTF16_TO_UTF8, a16)
 cases = [b"abc", b"\xc3\xa9", b"\xe2\x82", "🙂".encode() * 300, b""]
 lu.transcode_batch(lu.UTF8_TO_UTF16, cases)
 lu.validate_batch(lu.UTF8_TO_UTF16, cases)
