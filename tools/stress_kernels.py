@@ -44,13 +44,13 @@ def main():
     n = args.mib << 20
     out16 = torch.empty(n, dtype=torch.uint16, device=dev)
     out8 = torch.empty(3 * n // 2, dtype=torch.uint8, device=dev)
-    profiles = ("latin", "cyrillic", "cjk", "emoji")
+    profiles = ("latin", "cyrillic", "cjk", "emoji", "ascii")
     rates = (0.0, 1e-7, 1e-6, 1e-5, 1e-3)
     launches = 0
     t0 = time.time()
     for it in range(args.iters):
-        prof = profiles[it % 4]
-        rate = rates[(it // 4) % len(rates)]
+        prof = profiles[it % len(profiles)]
+        rate = rates[(it // len(profiles)) % len(rates)]
         for utf16 in (False, True):
             units = n // 2 if utf16 else n
             buf = corpus.generate(prof, units, 1000 + it, utf16=utf16, device=dev)
@@ -73,10 +73,11 @@ def main():
     import random
 
     rng = random.Random(args.seed)
-    base8 = corpus.generate("mix", n + 64, 77, device=dev)
-    base16 = corpus.generate("mix", n // 2 + 64, 78, utf16=True, device=dev)
+    bases8 = [corpus.generate(p, n + 64, 77, device=dev) for p in ("mix", "ascii")]
+    bases16 = [corpus.generate(p, n // 2 + 64, 78, utf16=True, device=dev) for p in ("mix", "ascii")]
     for it in range(args.random_iters):
         utf16 = bool(it & 1)
+        base8, base16 = bases8[(it >> 1) & 1], bases16[(it >> 1) & 1]
         units = rng.choice([1, 7, 100, 4096, 65536, 1 << 20, (1 << 20) + 3, rng.randrange(1, n // 2 if utf16 else n)])
         lead = rng.randrange(0, 16)
         # a view at an odd offset: misaligned input pointers (the kernels
