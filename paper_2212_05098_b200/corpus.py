@@ -100,6 +100,10 @@ PROFILES = {
     "cyrillic": Profile("cyrillic", (_Class(0.20, pool=_PUNCT), _Class(0.80, 0x0400, 0x04FF))),
     "cjk": Profile("cjk", (_Class(0.10, pool=_LETTERS + _DIGITS), _Class(0.90, 0x4E00, 0x9FFF))),
     "emoji": Profile("emoji", (_Class(0.50, pool=_LETTERS), _Class(0.50, 0x1F300, 0x1FAFF))),
+    # accented Latin with typographic punctuation / currency signs: ASCII + 2-byte + 3-byte
+    # in every 2 KiB chunk (no single class path; the validators' BMP class)
+    "typo": Profile("typo", (_Class(0.85, pool=_LETTERS + _PUNCT), _Class(0.10, 0x00C0, 0x017F),
+                             _Class(0.05, 0x2010, 0x20AC))),
     # plain ASCII text (the paper's ASCII fast path; exercises the kernels' ASCII chunk path)
     "ascii": Profile("ascii", (_Class(1.0, pool=_LETTERS + _PUNCT + _DIGITS),)),
     # config 1: uniform within each UTF-8 length class, no word structure

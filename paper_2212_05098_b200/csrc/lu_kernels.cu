@@ -1034,6 +1034,8 @@ __global__ void __launch_bounds__(kThreads, LU_LC_CTAS) k_validate8_lc(const uin
                     fd = lc_detect<1, Count>(x, xp, xn, c_nc, c_nf);
                 else if (hint == 3)
                     fd = lc_detect<3, Count>(x, xp, xn, c_nc, c_nf);
+                else if (hint == (uint32_t)kLcBmp)
+                    fd = lc_detect<kLcBmp, Count>(x, xp, xn, c_nc, c_nf);
                 if (__any_sync(0xffffffffu, fd != 0)) {
                     // class miss: the exact general detector on the same registers
                     uint32_t cls = 0;

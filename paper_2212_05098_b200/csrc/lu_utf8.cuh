@@ -32,6 +32,9 @@
 #ifndef LU_ONE_VOTE
 #define LU_ONE_VOTE 1
 #endif
+#ifndef LU_K1_CHUNK3
+#define LU_K1_CHUNK3 1 // K1: straight-line chunks for class 3 (ASCII + 4-byte) too
+#endif
 #ifndef LU_MERGED_TERMS
 #define LU_MERGED_TERMS 1
 #endif
@@ -141,7 +144,13 @@ struct U8Round {
     uint32_t key[5]; // path 3 (fast): per byte plane - 1 of a 4-byte lead (u8_plane_m1), quads 1..4
     uint32_t det;    // nonzero: a bad byte may lie in this lane's 16 bytes
     int path;
+    uint32_t next;   // u8_round_detect: the class hint for the warp's next round (path, or kHintBmp)
 };
+
+// Class hint beyond the paths 0..3: ASCII + 2-byte + 3-byte leads, no F-class
+// byte and no E0 / ED lead (BMP text of mixed scripts, e.g. accented Latin with
+// typographic punctuation or currency signs): u8_fast01 / u8u16_round<kHintBmp>.
+constexpr uint32_t kHintBmp = 5;
 
 // E0 80..9F (overlong) / ED A0..BF (surrogate): u = (b&0xF)<<1 | bit5(c1) in {0, 27}
 __device__ __forceinline__ uint32_t u8_check_e(uint32_t x, uint32_t n1, const U8Masks &c)
@@ -187,6 +196,7 @@ __device__ __forceinline__ void u8_round_detect(U8Round &R)
     uint32_t det = 0;
     if (!__any_sync(0xffffffffu, anye != 0)) {
         R.path = 0;
+        R.next = 0;
 #pragma unroll
         for (int k = 1; k <= 4; ++k) {
             const U8Masks &c = R.m[k];
@@ -206,6 +216,7 @@ __device__ __forceinline__ void u8_round_detect(U8Round &R)
     }
     if (!__any_sync(0xffffffffu, (anyf | any2) != 0)) {
         R.path = 1;
+        R.next = 1;
         uint32_t pe = 0;
 #pragma unroll
         for (int k = 1; k <= 4; ++k) {
@@ -227,6 +238,7 @@ __device__ __forceinline__ void u8_round_detect(U8Round &R)
         any3 |= R.m[k].E & ~R.m[k].F;
     if (!__any_sync(0xffffffffu, (any2 | any3) != 0)) {
         R.path = 3;
+        R.next = 3;
 #pragma unroll
         for (int k = 1; k <= 4; ++k) {
             const U8Masks &c = R.m[k], &p = R.m[k - 1];
@@ -246,7 +258,9 @@ __device__ __forceinline__ void u8_round_detect(U8Round &R)
         det |= c.L & ~c.E & ~((x & 0x1E1E1E1Eu) + 0x7F7F7F7Fu); // C0 / C1
         pe |= u8_prefilter_e(x, c);
     }
+    R.next = kHintBmp; // no F-class byte and no E0 / ED lead in the round: the BMP class next time
     if (__any_sync(0xffffffffu, (pe | anyf) != 0)) {
+        R.next = 2;
 #pragma unroll
         for (int k = 1; k <= 4; ++k) {
             const uint32_t n1 = fsr(R.w[k], R.w[k + 1], 8);
@@ -379,6 +393,38 @@ __device__ __forceinline__ uint32_t u8_fast3(U8Round &R)
         R.m[k].L = F;
         R.m[k].E = F;
         R.m[k].F = F;
+    }
+    return det & H8;
+}
+
+// BMP class (kHintBmp): ASCII, 2-byte and 3-byte leads; flags F-class bytes and
+// E0 / ED candidates (so no second-byte range check is needed), C0 / C1 and
+// every continuation the leads do not claim
+__device__ __forceinline__ uint32_t u8_fast01(U8Round &R)
+{
+    uint32_t Lp, Ep;
+    {
+        const uint32_t x = R.w[0];
+        Lp = x & (x << 1) & H8;
+        Ep = Lp & (x << 2);
+    }
+    uint32_t det = 0;
+#pragma unroll
+    for (int k = 1; k <= 4; ++k) {
+        const uint32_t x = R.w[k];
+        const uint32_t t1 = x << 1, t2 = x << 2;
+        const uint32_t C = x & ~t1 & H8, L = x & t1 & H8;
+        const uint32_t E = L & t2;
+        det |= (fsl(Lp, L, 8) | fsl(Ep, E, 16)) ^ C;
+        det |= L & ~t2 & ~((x & 0x1E1E1E1Eu) + 0x7F7F7F7Fu); // C0 / C1
+        const uint32_t u = x + 0x03030303u;                   // E0 / ED candidates (u8_prefilter_e)
+        det |= E & ((x << 3) | ~((u << 4) | (u << 5)));       // an F-class byte or a candidate
+        R.m[k].C = C;
+        R.m[k].L = L;
+        R.m[k].E = E;
+        R.m[k].F = 0;
+        Lp = L;
+        Ep = E;
     }
     return det & H8;
 }
@@ -531,7 +577,7 @@ __device__ __forceinline__ void u8u16_round(const U8Round &R, int r, const uint8
     uint32_t e[4], fi1[4], c[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        if (P >= 2) {
+        if (P == 2 || P == 3) {
             fi1[k] = fsl(R.m[k].F, R.m[k + 1].F, 8);
             e[k] = (~R.m[k + 1].C | fi1[k]) & H8;
         } else {
@@ -628,6 +674,10 @@ __device__ __forceinline__ void u8u16_round(const U8Round &R, int r, const uint8
 #pragma unroll
         for (int k = 0; k < 4; ++k)
             u8_decode4(R.w[k + 1], R.w[k + 2], R.m[k + 1], R.key[k + 1], lop[k], hip[k]);
+    } else if (P == (int)kHintBmp) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            u8_decode_quad(R.w[k + 1], R.w[k + 2], R.m[k + 1], 0u, false, lop[k], hip[k]);
     } else {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
@@ -772,10 +822,12 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
         hint = 0;
     }
 
-    if (!Boundary && hint < 2) {
+    if (!Boundary && (hint < 2 || (LU_K1_CHUNK3 && hint == 3))) {
         uint32_t miss;
         if (hint == 0)
             miss = u8u16_chunk_fast<0, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
+        else if (LU_K1_CHUNK3 && hint == 3)
+            miss = u8u16_chunk_fast<3, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
         else
             miss = u8u16_chunk_fast<1, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
         if (!miss) {
@@ -821,11 +873,11 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
         }                                                                                                              \
     }
         LU_FAST_ROUND(0, u8_fast0)
-        else LU_FAST_ROUND(1, u8_fast1) else LU_FAST_ROUND(3, u8_fast3)
+        else LU_FAST_ROUND(1, u8_fast1) else LU_FAST_ROUND(3, u8_fast3) else LU_FAST_ROUND(kHintBmp, u8_fast01)
 #undef LU_FAST_ROUND
         if (!fast) {
             u8_round_detect(R);
-            hint = (uint32_t)R.path;
+            hint = R.next;
             if (r == kRounds - 1 && lane == 31)
                 R.det |= u8_chunk_end_check(R);
             u8u16_round<2, Boundary, BE>(R, r, base, tile_off, chunk, lane_off, lo_b, hi_b, sbase, sel, running, err,

@@ -25,6 +25,9 @@ namespace lu {
 #endif
 
 constexpr int kLcQuads = kChunkBytes / 128; // quads per lane (16)
+// class hint beyond the class paths 0..3: ASCII + 2-byte + 3-byte leads, no
+// F-class byte (kHintBmp, lu_utf8.cuh)
+constexpr int kLcBmp = (int)kHintBmp;
 
 // a * b + c as one integer multiply-add (IMAD: the FMA pipe, which these
 // ALU-bound detectors leave half idle); opaque to the optimiser so it is not
@@ -123,6 +126,28 @@ __device__ __forceinline__ uint32_t lc_detect(const uint32_t (&x)[kLcQuads], uin
             }
         }
         det |= lc_end_check(C, F, F, F, xn);
+    } else if (P == kLcBmp) {
+        // ASCII, 2-byte and 3-byte leads (BMP text of mixed scripts, e.g.
+        // accented Latin with typographic punctuation): flags F-class bytes and
+        // E0 / ED candidates, so no second-byte range check is needed
+        uint32_t Lp = xp & (xp << 1) & H8, Ep = Lp & (xp << 2), C = 0, L = 0, E = 0;
+#pragma unroll
+        for (int k = 0; k < kLcQuads; ++k) {
+            const uint32_t v = x[k];
+            const uint32_t t1 = v << 1, t2 = v << 2;
+            C = v & ~t1 & H8;
+            L = v & t1 & H8;
+            E = L & t2;
+            det |= (fsl(Lp, L, 8) | fsl(Ep, E, 16)) ^ C;
+            det |= L & ~t2 & ~((v & 0x1E1E1E1Eu) + 0x7F7F7F7Fu); // C0 / C1
+            const uint32_t u = v + 0x03030303u;                   // E0 / ED candidates (u8_prefilter_e)
+            det |= E & ((v << 3) | ~((u << 4) | (u << 5)));       // an F-class byte or a candidate
+            if (Count)
+                nc = __dp4a(C, 0x01010101u, nc);
+            Lp = L;
+            Ep = E;
+        }
+        det |= lc_end_check(C, L, E, 0u, xn);
     }
     return det & H8;
 }
@@ -168,6 +193,8 @@ __device__ __forceinline__ uint32_t lc_path_of(uint32_t cls)
         return 1; // 3-byte leads only
     if (cls == 4u)
         return 3; // 4-byte leads only
+    if (cls == 3u)
+        return kLcBmp; // 2- and 3-byte leads, no F-class byte
     return 2;
 }
 

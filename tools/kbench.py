@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2212_05098_b200 import UTF8_TO_UTF16, UTF16_TO_UTF8, _native, corpus, outcome_from_tensor  # noqa: E402
 from paper_2212_05098_b200 import count_device, transcode_device, validate_device  # noqa: E402
 
-PROFILES = (("latin", 1), ("cyrillic", 2), ("cjk", 3), ("emoji", 4), ("ascii", 5), ("mix", 0))
+PROFILES = (("latin", 1), ("cyrillic", 2), ("cjk", 3), ("emoji", 4), ("ascii", 5), ("mix", 0), ("typo", 6))
 
 
 def main():
@@ -62,7 +62,7 @@ def main():
         assert o.ok, o
         report[f"k2_{p}"] = {"us": round(t * 1e6, 1), "gib_s": round(n / t / 2**30, 1),
                              "frac": round((n + o.written) / t / 1e9 / peak, 3)}
-        if p in ("cjk", "emoji", "ascii", "mix"):
+        if p in ("cjk", "emoji", "ascii", "mix", "typo"):
             t = timeit(lambda: validate_device(UTF8_TO_UTF16, u8, res=res, ws=ws))
             report[f"k3_{p}"] = {"us": round(t * 1e6, 1), "gib_s": round(n / t / 2**30, 1),
                                  "frac": round(n / t / 1e9 / peak, 3)}
