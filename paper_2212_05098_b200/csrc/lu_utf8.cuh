@@ -32,6 +32,9 @@
 #ifndef LU_ONE_VOTE
 #define LU_ONE_VOTE 1
 #endif
+#ifndef LU_K1_CHUNK5
+#define LU_K1_CHUNK5 1 // ... and for the BMP class
+#endif
 #ifndef LU_K1_CHUNK3
 #define LU_K1_CHUNK3 1 // K1: straight-line chunks for class 3 (ASCII + 4-byte) too
 #endif
@@ -753,7 +756,7 @@ __device__ __forceinline__ uint32_t u8u16_chunk_fast(const uint8_t *__restrict__
         R.w[3] = q[r].z;
         R.w[4] = q[r].w;
         R.w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : in.halo_n) : rn[r];
-        uint32_t fd = P == 0 ? u8_fast0(R) : P == 1 ? u8_fast1(R) : u8_fast3(R);
+        uint32_t fd = P == 0 ? u8_fast0(R) : P == 1 ? u8_fast1(R) : P == 3 ? u8_fast3(R) : u8_fast01(R);
         if (r == kRounds - 1 && lane == 31)
             fd |= u8_chunk_end_check(R);
 #if LU_ONE_VOTE
@@ -822,12 +825,14 @@ __device__ __forceinline__ void u8u16_warp(const uint8_t *__restrict__ base, int
         hint = 0;
     }
 
-    if (!Boundary && (hint < 2 || (LU_K1_CHUNK3 && hint == 3))) {
+    if (!Boundary && (hint < 2 || (LU_K1_CHUNK3 && hint == 3) || (LU_K1_CHUNK5 && hint == kHintBmp))) {
         uint32_t miss;
         if (hint == 0)
             miss = u8u16_chunk_fast<0, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
         else if (LU_K1_CHUNK3 && hint == 3)
             miss = u8u16_chunk_fast<3, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
+        else if (LU_K1_CHUNK5 && hint == kHintBmp)
+            miss = u8u16_chunk_fast<(int)kHintBmp, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
         else
             miss = u8u16_chunk_fast<1, BE>(base, tile_off, chunk, lo_b, hi_b, sbase, sel, in, rn, running);
         if (!miss) {
