@@ -198,6 +198,29 @@ __device__ __forceinline__ void sel_table_init(SelPair *sel)
         }
         sel[32 + idx].s01 = sel_v;
         sel[32 + idx].s23 = j; // byte count
+    } else if (threadIdx.x < 56) {
+        // K2 path D (no surrogate, words of 1, 2 or 3 bytes): entry c0 | c1 << 2
+        // with c = bytes - 1 of each word of a pair.  prmt bytes 0-3 =
+        // [X0, Y0, X1, Y1] (middle / last byte planes of the pair), bytes 4, 5 =
+        // Z0, Z1 (3-byte leads): s01 = selector of the pair's first four
+        // bytes, s23 = selector of bytes five and six | byte count << 16
+        const uint32_t idx = threadIdx.x - 40;
+        const uint32_t c0 = idx & 3u, c1 = idx >> 2;
+        uint32_t b[6] = {0, 0, 0, 0, 0, 0}, j = 0;
+        if (c0 < 3 && c1 < 3) {
+            if (c0 == 2)
+                b[j++] = 4;
+            if (c0 >= 1)
+                b[j++] = 0;
+            b[j++] = 1;
+            if (c1 == 2)
+                b[j++] = 5;
+            if (c1 >= 1)
+                b[j++] = 2;
+            b[j++] = 3;
+        }
+        sel[40 + idx].s01 = b[0] | b[1] << 4 | b[2] << 8 | b[3] << 12;
+        sel[40 + idx].s23 = b[4] | b[5] << 4 | j << 16;
     }
 }
 
@@ -521,7 +544,7 @@ __global__ void __launch_bounds__(kPipeThreads, 3)
 {
     using OutT = typename Dir::OutT;
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    __shared__ SelPair sel[40]; // K1 compaction selectors, then K2 path-C and path-A selectors
+    __shared__ SelPair sel[56]; // K1 compaction selectors, then K2 path-C, path-A and path-D selectors
     __shared__ GroupShared gshared[kGroupsPerCta];
     __shared__ ScanShared scan_s;
     __shared__ uint32_t role_s;
@@ -1140,7 +1163,7 @@ __global__ void __launch_bounds__(kThreads) k_batch(const uint8_t *__restrict__ 
     constexpr bool kUtf16 = (Op == 1 || Op == 3);
     constexpr int kShift = kUtf16 ? 1 : 0;
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    __shared__ SelPair sel[40];
+    __shared__ SelPair sel[56];
     __shared__ WarpResult wres[kWarps];
     sel_table_init(sel);
     __syncthreads();

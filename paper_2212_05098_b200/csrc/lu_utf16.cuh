@@ -128,6 +128,9 @@ __device__ __forceinline__ void sts16b_if(uint32_t addr, uint32_t v, uint32_t n,
 #ifndef LU_K2_ASCII
 #define LU_K2_ASCII 1
 #endif
+#ifndef LU_K2_PATH_D
+#define LU_K2_PATH_D 1 // SWAR path for rounds without surrogates that mix 1-, 2- and 3-byte words
+#endif
 
 // ASCII chunk (every word < 0x80): one vote, then the words' low bytes are
 // packed straight into the staging region (one 8-byte store per round) -- no
@@ -411,6 +414,59 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
             running += __shfl_sync(0xffffffffu, incl, 31);
             continue;
         }
+        if (LU_K2_PATH_D && !Boundary && !sur) {
+            // path D (warp-uniform, interior chunks): no surrogate, words of
+            // 1, 2 and 3 bytes mixed (BMP text of mixed scripts).  Per word
+            // the UTF-8 string is the last len bytes of (Z', X', Y'):
+            //   Z' = E0 | w >> 12,  X' = (80 or C0) | (w >> 6) & 3F,  Y' = 80 | w & 3F (ASCII: w)
+            // built as byte planes on the gathered high / low bytes (4 words
+            // per op); per word pair two prmt through a 9-entry selector table
+            uint32_t T[4], Z[2], cl[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const uint32_t hb = hi_bytes(w[2 * j + 1], w[2 * j + 2]), lb = lo_bytes(w[2 * j + 1], w[2 * j + 2]);
+                const uint32_t z = hb | (lb & H8);
+                const uint32_t big = (((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) & H8;  // word >= 0x80
+                const uint32_t mid = (((hb & 0x78787878u) + 0x7F7F7F7Fu) | hb) & H8; // word >= 0x800
+                const uint32_t m = sgn8(big);
+                const uint32_t X = ((hb << 2) & 0x3C3C3C3Cu) | ((lb >> 6) & 0x03030303u) | H8 | ((~mid & H8) >> 1);
+                const uint32_t Y = (lb & ~m) | (((lb & 0x3F3F3F3Fu) | H8) & m);
+                Z[j] = ((hb >> 4) & 0x0F0F0F0Fu) | 0xE0E0E0E0u;
+                T[2 * j] = prmt(X, Y, 0x5140u);     // [X0, Y0, X1, Y1]
+                T[2 * j + 1] = prmt(X, Y, 0x7362u); // [X2, Y2, X3, Y3]
+                cl[j] = (big >> 7) + (mid >> 7);     // bytes - 1 per word (0..2)
+            }
+            const char *selb = reinterpret_cast<const char *>(sel) + 192;
+            uint32_t pl[4], ph[4], nb[4], cnt = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t c = cl[k >> 1] >> (16 * (k & 1));
+                // byte offset (idx * 8) of idx = c0 | c1 << 2 (c in bytes 0 and 1)
+                const uint32_t bo = ((c & 0x3u) | ((c >> 6) & 0xCu)) << 3;
+                const SelPair sp = *reinterpret_cast<const SelPair *>(selb + bo);
+                const uint32_t zz = Z[k >> 1] >> (16 * (k & 1));
+                pl[k] = prmt(T[k], zz, sp.s01);
+                ph[k] = prmt(T[k], zz, sp.s23);
+                nb[k] = sp.s23 >> 16;
+                cnt += nb[k];
+            }
+            const uint32_t incl = warp_incl_scan(cnt);
+            uint32_t off = running + incl - cnt;
+            // 2..6 bytes per quad
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t a = sbase + off;
+                sts8(a, pl[k]);
+                sts8(a + 1, pl[k] >> 8);
+                sts8_if(a + 2, pl[k] >> 16, nb[k], 2);
+                sts8_if(a + 3, pl[k] >> 24, nb[k], 3);
+                sts8_if(a + 4, ph[k], nb[k], 4);
+                sts8_if(a + 5, ph[k] >> 8, nb[k], 5);
+                off += nb[k];
+            }
+            running += __shfl_sync(0xffffffffu, incl, 31);
+            continue;
+        }
         uint32_t lo[4], hi[4], n[4], bad[4];
         uint32_t cnt = 0, anybad = 0;
 #pragma unroll
@@ -418,7 +474,8 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
             const uint32_t x = w[k + 1];
             const uint32_t w0 = x & 0xFFFFu, w1 = x >> 16, wp = w[k] >> 16, wn = w[k + 2] & 0xFFFFu;
             uint32_t u0, l0, u1, l1;
-            if (sur) {
+            // (interior chunks: rounds without surrogates took path A, B or D above)
+            if ((LU_K2_PATH_D && !Boundary) || sur) {
                 u16_encode(w0, wp, w1, u0, l0);
                 u16_encode(w1, w0, wn, u1, l1);
                 bad[k] = u16_bad2(w0, w1, wp, wn);
@@ -455,7 +512,7 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
         const uint32_t incl = warp_incl_scan(cnt);
         const uint32_t excl = incl - cnt;
         const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-        if (sur && __any_sync(0xffffffffu, anybad != 0)) {
+        if (((LU_K2_PATH_D && !Boundary) || sur) && __any_sync(0xffffffffu, anybad != 0)) {
             uint32_t kb = 8, within = excl;
 #pragma unroll
             for (int k = 3; k >= 0; --k)
