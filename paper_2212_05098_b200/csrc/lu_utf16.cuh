@@ -153,6 +153,66 @@ __device__ __noinline__ bool u16u8_ascii_chunk(uint4 q0, uint4 q1, uint4 q2, uin
     return true;
 }
 
+// Path D of the K2 warp body, out of line (the round loop is unrolled four
+// times; inlined, this path cost the single-class profiles 1-3%): one round
+// without surrogates whose words mix 1, 2 and 3 bytes.  w1..w4 the lane's four
+// quads; returns the warp's running byte offset after the round.
+__device__ __noinline__ uint32_t u16u8_round_d(uint32_t w1, uint32_t w2, uint32_t w3, uint32_t w4, uint32_t sbase,
+                                               uint32_t running, const SelPair *sel)
+{
+    const uint32_t w[5] = {0u, w1, w2, w3, w4};
+            // path D (warp-uniform, interior chunks): no surrogate, words of
+            // 1, 2 and 3 bytes mixed (BMP text of mixed scripts).  Per word
+            // the UTF-8 string is the last len bytes of (Z', X', Y'):
+            //   Z' = E0 | w >> 12,  X' = (80 or C0) | (w >> 6) & 3F,  Y' = 80 | w & 3F (ASCII: w)
+            // built as byte planes on the gathered high / low bytes (4 words
+            // per op); per word pair two prmt through a 9-entry selector table
+            uint32_t T[4], Z[2], cl[2];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const uint32_t hb = hi_bytes(w[2 * j + 1], w[2 * j + 2]), lb = lo_bytes(w[2 * j + 1], w[2 * j + 2]);
+                const uint32_t z = hb | (lb & H8);
+                const uint32_t big = (((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) & H8;  // word >= 0x80
+                const uint32_t mid = (((hb & 0x78787878u) + 0x7F7F7F7Fu) | hb) & H8; // word >= 0x800
+                const uint32_t m = sgn8(big);
+                const uint32_t X = ((hb << 2) & 0x3C3C3C3Cu) | ((lb >> 6) & 0x03030303u) | H8 | ((~mid & H8) >> 1);
+                const uint32_t Y = (lb & ~m) | (((lb & 0x3F3F3F3Fu) | H8) & m);
+                Z[j] = ((hb >> 4) & 0x0F0F0F0Fu) | 0xE0E0E0E0u;
+                T[2 * j] = prmt(X, Y, 0x5140u);     // [X0, Y0, X1, Y1]
+                T[2 * j + 1] = prmt(X, Y, 0x7362u); // [X2, Y2, X3, Y3]
+                cl[j] = (big >> 7) + (mid >> 7);     // bytes - 1 per word (0..2)
+            }
+            const char *selb = reinterpret_cast<const char *>(sel) + 192;
+            uint32_t pl[4], ph[4], nb[4], cnt = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t c = cl[k >> 1] >> (16 * (k & 1));
+                // byte offset (idx * 8) of idx = c0 | c1 << 2 (c in bytes 0 and 1)
+                const uint32_t bo = ((c & 0x3u) | ((c >> 6) & 0xCu)) << 3;
+                const SelPair sp = *reinterpret_cast<const SelPair *>(selb + bo);
+                const uint32_t zz = Z[k >> 1] >> (16 * (k & 1));
+                pl[k] = prmt(T[k], zz, sp.s01);
+                ph[k] = prmt(T[k], zz, sp.s23);
+                nb[k] = sp.s23 >> 16;
+                cnt += nb[k];
+            }
+            const uint32_t incl = warp_incl_scan(cnt);
+            uint32_t off = running + incl - cnt;
+            // 2..6 bytes per quad
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t a = sbase + off;
+                sts8(a, pl[k]);
+                sts8(a + 1, pl[k] >> 8);
+                sts8_if(a + 2, pl[k] >> 16, nb[k], 2);
+                sts8_if(a + 3, pl[k] >> 24, nb[k], 3);
+                sts8_if(a + 4, ph[k], nb[k], 4);
+                sts8_if(a + 5, ph[k] >> 8, nb[k], 5);
+                off += nb[k];
+            }
+            return running + __shfl_sync(0xffffffffu, incl, 31);
+}
+
 // K2 warp body for the pipelined kernel: the warp's 2 KiB chunk (1024 words)
 // in 4 rounds of 512 B, lane l holding words [8l, 8l+8) of the round in
 // registers; neighbour words by shuffle.  Per word: pair-aware UTF-8 encode
@@ -415,56 +475,9 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
             continue;
         }
         if (LU_K2_PATH_D && !Boundary && !sur) {
-            // path D (warp-uniform, interior chunks): no surrogate, words of
-            // 1, 2 and 3 bytes mixed (BMP text of mixed scripts).  Per word
-            // the UTF-8 string is the last len bytes of (Z', X', Y'):
-            //   Z' = E0 | w >> 12,  X' = (80 or C0) | (w >> 6) & 3F,  Y' = 80 | w & 3F (ASCII: w)
-            // built as byte planes on the gathered high / low bytes (4 words
-            // per op); per word pair two prmt through a 9-entry selector table
-            uint32_t T[4], Z[2], cl[2];
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const uint32_t hb = hi_bytes(w[2 * j + 1], w[2 * j + 2]), lb = lo_bytes(w[2 * j + 1], w[2 * j + 2]);
-                const uint32_t z = hb | (lb & H8);
-                const uint32_t big = (((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) & H8;  // word >= 0x80
-                const uint32_t mid = (((hb & 0x78787878u) + 0x7F7F7F7Fu) | hb) & H8; // word >= 0x800
-                const uint32_t m = sgn8(big);
-                const uint32_t X = ((hb << 2) & 0x3C3C3C3Cu) | ((lb >> 6) & 0x03030303u) | H8 | ((~mid & H8) >> 1);
-                const uint32_t Y = (lb & ~m) | (((lb & 0x3F3F3F3Fu) | H8) & m);
-                Z[j] = ((hb >> 4) & 0x0F0F0F0Fu) | 0xE0E0E0E0u;
-                T[2 * j] = prmt(X, Y, 0x5140u);     // [X0, Y0, X1, Y1]
-                T[2 * j + 1] = prmt(X, Y, 0x7362u); // [X2, Y2, X3, Y3]
-                cl[j] = (big >> 7) + (mid >> 7);     // bytes - 1 per word (0..2)
-            }
-            const char *selb = reinterpret_cast<const char *>(sel) + 192;
-            uint32_t pl[4], ph[4], nb[4], cnt = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t c = cl[k >> 1] >> (16 * (k & 1));
-                // byte offset (idx * 8) of idx = c0 | c1 << 2 (c in bytes 0 and 1)
-                const uint32_t bo = ((c & 0x3u) | ((c >> 6) & 0xCu)) << 3;
-                const SelPair sp = *reinterpret_cast<const SelPair *>(selb + bo);
-                const uint32_t zz = Z[k >> 1] >> (16 * (k & 1));
-                pl[k] = prmt(T[k], zz, sp.s01);
-                ph[k] = prmt(T[k], zz, sp.s23);
-                nb[k] = sp.s23 >> 16;
-                cnt += nb[k];
-            }
-            const uint32_t incl = warp_incl_scan(cnt);
-            uint32_t off = running + incl - cnt;
-            // 2..6 bytes per quad
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t a = sbase + off;
-                sts8(a, pl[k]);
-                sts8(a + 1, pl[k] >> 8);
-                sts8_if(a + 2, pl[k] >> 16, nb[k], 2);
-                sts8_if(a + 3, pl[k] >> 24, nb[k], 3);
-                sts8_if(a + 4, ph[k], nb[k], 4);
-                sts8_if(a + 5, ph[k] >> 8, nb[k], 5);
-                off += nb[k];
-            }
-            running += __shfl_sync(0xffffffffu, incl, 31);
+            // path D (warp-uniform, interior chunks): no surrogate, words of 1,
+            // 2 and 3 bytes mixed (BMP text of mixed scripts) -- u16u8_round_d
+            running = u16u8_round_d(w[1], w[2], w[3], w[4], sbase, running, sel);
             continue;
         }
         uint32_t lo[4], hi[4], n[4], bad[4];
