@@ -242,8 +242,11 @@ __device__ __forceinline__ void sel_table_init(SelPair *sel)
 // Named barriers per group g (kGroupThreads threads): 1+3g ticket broadcast,
 // 2+3g tile computed, 3+3g prefix broadcast.
 
-constexpr int kGroupWarps = 4;
-constexpr int kGroupsPerCta = 2;
+#ifndef LU_GROUP_WARPS
+#define LU_GROUP_WARPS 4
+#endif
+constexpr int kGroupWarps = LU_GROUP_WARPS;
+constexpr int kGroupsPerCta = 8 / kGroupWarps;
 constexpr int kGroupThreads = 32 * kGroupWarps;
 constexpr int kPipeTile = kGroupWarps * kChunkBytes; // 8 KiB
 constexpr int kPipeThreads = kGroupsPerCta * kGroupThreads;
@@ -421,12 +424,12 @@ __device__ __forceinline__ void group_combine(GroupShared &ps, uint32_t buf, uin
     const uint32_t first = errm ? (uint32_t)__ffs(errm) - 1 : kGroupWarps;
     const uint32_t u = (lane < kGroupWarps && lane <= first) ? r.units : 0u;
     uint32_t inc = u;
-    uint32_t o = __shfl_up_sync(0xffffffffu, inc, 1);
-    if (lane >= 1)
-        inc += o;
-    o = __shfl_up_sync(0xffffffffu, inc, 2);
-    if (lane >= 2)
-        inc += o;
+#pragma unroll
+    for (int d = 1; d < kGroupWarps; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= (uint32_t)d)
+            inc += o;
+    }
     if (lane < kGroupWarps)
         ps.warp_excl[buf][lane] = inc - u;
     const uint32_t units = __shfl_sync(0xffffffffu, inc, kGroupWarps - 1);
@@ -512,8 +515,14 @@ __device__ __forceinline__ void small_tile(GroupShared &ps, uint32_t tile, uint3
     }
     bar_sync(bar_prefix, kGroupThreads);
     if (gtid == 0) {
-        const unsigned long long sum = lb_sum[0] + lb_sum[1] + lb_sum[2] + lb_sum[3];
-        const bool e = (lb_err[0] | lb_err[1] | lb_err[2] | lb_err[3]) != 0;
+        unsigned long long sum = 0;
+        uint32_t eor = 0;
+#pragma unroll
+        for (int k = 0; k < kGroupWarps; ++k) {
+            sum += lb_sum[k];
+            eor |= lb_err[k];
+        }
+        const bool e = eor != 0;
         const uint64_t ex = (sum & kValMask) | (e ? kErrBit : 0ull);
         ps.excl[0] = ex;
         if (!e) {
