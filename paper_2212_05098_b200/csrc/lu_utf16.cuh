@@ -153,6 +153,108 @@ __device__ __noinline__ bool u16u8_ascii_chunk(uint4 q0, uint4 q1, uint4 q2, uin
     return true;
 }
 
+// General round of the K2 warp body, out of line (keeps the unrolled round
+// loop small: interior chunks only come here for rounds with surrogates that
+// are not path C, i.e. malformed or mixed with BMP words; boundary chunks for
+// every round): per-word pair-aware encode (u16_encode), exact local error
+// predicate (u16_bad2), seven predicated byte stores per word pair.  w0..w5 =
+// the quad before, the lane's four quads, the quad after (by value: an array
+// argument would pin the caller's quads in local memory).  Returns {running
+// after the round, err, round-relative err_pos, units before the error}.
+template <bool Boundary>
+__device__ __noinline__ uint4 u16u8_round_general(uint32_t w0_, uint32_t w1_, uint32_t w2_, uint32_t w3_, uint32_t w4_,
+                                                  uint32_t w5_, bool sur, int64_t lane_off, int64_t lo_b, int64_t hi_b,
+                                                  uint32_t sbase, uint32_t running)
+{
+    const uint32_t w[6] = {w0_, w1_, w2_, w3_, w4_, w5_};
+    uint32_t err = 0, err_pos = 0, units = 0;
+        uint32_t lo[4], hi[4], n[4], bad[4];
+        uint32_t cnt = 0, anybad = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t x = w[k + 1];
+            const uint32_t w0 = x & 0xFFFFu, w1 = x >> 16, wp = w[k] >> 16, wn = w[k + 2] & 0xFFFFu;
+            uint32_t u0, l0, u1, l1;
+            // (interior chunks: rounds without surrogates took path A, B or D above)
+            if ((LU_K2_PATH_D && !Boundary) || sur) {
+                u16_encode(w0, wp, w1, u0, l0);
+                u16_encode(w1, w0, wn, u1, l1);
+                bad[k] = u16_bad2(w0, w1, wp, wn);
+            } else {
+                // no surrogates in the round: 1-3 bytes per word, never an error
+                u0 = w0 < 0x80u ? w0
+                     : w0 < 0x800u ? (0xC0u | (w0 >> 6)) | ((0x80u | (w0 & 0x3Fu)) << 8)
+                                   : (0xE0u | (w0 >> 12)) | ((0x80u | ((w0 >> 6) & 0x3Fu)) << 8) |
+                                         ((0x80u | (w0 & 0x3Fu)) << 16);
+                l0 = 1u + (w0 >= 0x80u) + (w0 >= 0x800u);
+                u1 = w1 < 0x80u ? w1
+                     : w1 < 0x800u ? (0xC0u | (w1 >> 6)) | ((0x80u | (w1 & 0x3Fu)) << 8)
+                                   : (0xE0u | (w1 >> 12)) | ((0x80u | ((w1 >> 6) & 0x3Fu)) << 8) |
+                                         ((0x80u | (w1 & 0x3Fu)) << 16);
+                l1 = 1u + (w1 >= 0x80u) + (w1 >= 0x800u);
+                bad[k] = 0;
+            }
+            if (Boundary) {
+                const uint32_t v = valid_words(lane_off + 4 * k, lo_b, hi_b);
+                if (!(v & 1))
+                    l0 = 0;
+                if (!(v & 2))
+                    l1 = 0;
+                bad[k] &= v;
+            }
+            // l0 <= 4 and u1 < 2^32, so the pair packs into 64 bits
+            const uint64_t p = (uint64_t)u0 | ((uint64_t)u1 << (8 * l0));
+            lo[k] = (uint32_t)p;
+            hi[k] = (uint32_t)(p >> 32);
+            n[k] = (l0 + l1) | (l0 << 8); // total bytes | bytes of the low word
+            cnt += l0 + l1;
+            anybad |= bad[k];
+        }
+        const uint32_t incl = warp_incl_scan(cnt);
+        const uint32_t excl = incl - cnt;
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (((LU_K2_PATH_D && !Boundary) || sur) && __any_sync(0xffffffffu, anybad != 0)) {
+            uint32_t kb = 8, within = excl;
+#pragma unroll
+            for (int k = 3; k >= 0; --k)
+                if (bad[k]) {
+                    const uint32_t which = (bad[k] & 1) ? 0u : 1u;
+                    kb = 2 * k + which;
+                }
+            // bytes emitted before the first bad word of this lane
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t nk = n[k] & 0xFFu, l0k = n[k] >> 8;
+                if ((uint32_t)(2 * k + 1) < kb)
+                    within += nk;
+                else if ((uint32_t)(2 * k) < kb)
+                    within += l0k;
+            }
+            const uint32_t bm = __ballot_sync(0xffffffffu, kb < 8);
+            const uint32_t fl = (uint32_t)__ffs(bm) - 1;
+            const uint32_t kbf = __shfl_sync(0xffffffffu, kb, fl);
+            const uint32_t wf = __shfl_sync(0xffffffffu, within, fl);
+            err = 1;
+            err_pos = 16 * fl + 2 * kbf; // round-relative; the caller adds the round's offset
+            units = running + wf;
+        }
+        uint32_t off = running + excl;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t a = sbase + off;
+            const uint32_t nk = n[k] & 0xFFu;
+            sts8_if(a, lo[k], nk, 0);
+            sts8_if(a + 1, lo[k] >> 8, nk, 1);
+            sts8_if(a + 2, lo[k] >> 16, nk, 2);
+            sts8_if(a + 3, lo[k] >> 24, nk, 3);
+            sts8_if(a + 4, hi[k], nk, 4);
+            sts8_if(a + 5, hi[k] >> 8, nk, 5);
+            sts8_if(a + 6, hi[k] >> 16, nk, 6);
+            off += nk;
+        }
+        return make_uint4(running + tot, err, err_pos, units);
+}
+
 // Path D of the K2 warp body, out of line (the round loop is unrolled four
 // times; inlined, this path cost the single-class profiles 1-3%): one round
 // without surrogates whose words mix 1, 2 and 3 bytes.  w1..w4 the lane's four
@@ -480,91 +582,16 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
             running = u16u8_round_d(w[1], w[2], w[3], w[4], sbase, running, sel);
             continue;
         }
-        uint32_t lo[4], hi[4], n[4], bad[4];
-        uint32_t cnt = 0, anybad = 0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t x = w[k + 1];
-            const uint32_t w0 = x & 0xFFFFu, w1 = x >> 16, wp = w[k] >> 16, wn = w[k + 2] & 0xFFFFu;
-            uint32_t u0, l0, u1, l1;
-            // (interior chunks: rounds without surrogates took path A, B or D above)
-            if ((LU_K2_PATH_D && !Boundary) || sur) {
-                u16_encode(w0, wp, w1, u0, l0);
-                u16_encode(w1, w0, wn, u1, l1);
-                bad[k] = u16_bad2(w0, w1, wp, wn);
-            } else {
-                // no surrogates in the round: 1-3 bytes per word, never an error
-                u0 = w0 < 0x80u ? w0
-                     : w0 < 0x800u ? (0xC0u | (w0 >> 6)) | ((0x80u | (w0 & 0x3Fu)) << 8)
-                                   : (0xE0u | (w0 >> 12)) | ((0x80u | ((w0 >> 6) & 0x3Fu)) << 8) |
-                                         ((0x80u | (w0 & 0x3Fu)) << 16);
-                l0 = 1u + (w0 >= 0x80u) + (w0 >= 0x800u);
-                u1 = w1 < 0x80u ? w1
-                     : w1 < 0x800u ? (0xC0u | (w1 >> 6)) | ((0x80u | (w1 & 0x3Fu)) << 8)
-                                   : (0xE0u | (w1 >> 12)) | ((0x80u | ((w1 >> 6) & 0x3Fu)) << 8) |
-                                         ((0x80u | (w1 & 0x3Fu)) << 16);
-                l1 = 1u + (w1 >= 0x80u) + (w1 >= 0x800u);
-                bad[k] = 0;
+        {
+            const uint4 g = u16u8_round_general<Boundary>(w[0], w[1], w[2], w[3], w[4], w[5], sur, lane_off, lo_b, hi_b,
+                                                          sbase, running);
+            if (g.y) {
+                err = 1;
+                err_pos = (uint32_t)(chunk + r * 512 - tile_off) + g.z;
+                units = g.w;
             }
-            if (Boundary) {
-                const uint32_t v = valid_words(lane_off + 4 * k, lo_b, hi_b);
-                if (!(v & 1))
-                    l0 = 0;
-                if (!(v & 2))
-                    l1 = 0;
-                bad[k] &= v;
-            }
-            // l0 <= 4 and u1 < 2^32, so the pair packs into 64 bits
-            const uint64_t p = (uint64_t)u0 | ((uint64_t)u1 << (8 * l0));
-            lo[k] = (uint32_t)p;
-            hi[k] = (uint32_t)(p >> 32);
-            n[k] = (l0 + l1) | (l0 << 8); // total bytes | bytes of the low word
-            cnt += l0 + l1;
-            anybad |= bad[k];
+            running = g.x;
         }
-        const uint32_t incl = warp_incl_scan(cnt);
-        const uint32_t excl = incl - cnt;
-        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-        if (((LU_K2_PATH_D && !Boundary) || sur) && __any_sync(0xffffffffu, anybad != 0)) {
-            uint32_t kb = 8, within = excl;
-#pragma unroll
-            for (int k = 3; k >= 0; --k)
-                if (bad[k]) {
-                    const uint32_t which = (bad[k] & 1) ? 0u : 1u;
-                    kb = 2 * k + which;
-                }
-            // bytes emitted before the first bad word of this lane
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t nk = n[k] & 0xFFu, l0k = n[k] >> 8;
-                if ((uint32_t)(2 * k + 1) < kb)
-                    within += nk;
-                else if ((uint32_t)(2 * k) < kb)
-                    within += l0k;
-            }
-            const uint32_t bm = __ballot_sync(0xffffffffu, kb < 8);
-            const uint32_t fl = (uint32_t)__ffs(bm) - 1;
-            const uint32_t kbf = __shfl_sync(0xffffffffu, kb, fl);
-            const uint32_t wf = __shfl_sync(0xffffffffu, within, fl);
-            err = 1;
-            err_pos = (uint32_t)(chunk + r * 512 - tile_off) + 16 * fl + 2 * kbf;
-            units = running + wf;
-        }
-        uint32_t off = running + excl;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t a = sbase + off;
-            const uint32_t nk = n[k] & 0xFFu;
-            sts8_if(a, lo[k], nk, 0);
-            sts8_if(a + 1, lo[k] >> 8, nk, 1);
-            sts8_if(a + 2, lo[k] >> 16, nk, 2);
-            sts8_if(a + 3, lo[k] >> 24, nk, 3);
-            sts8_if(a + 4, hi[k], nk, 4);
-            sts8_if(a + 5, hi[k] >> 8, nk, 5);
-            sts8_if(a + 6, hi[k] >> 16, nk, 6);
-            off += nk;
-        }
-        running += tot;
         if (err)
             break;
     }
