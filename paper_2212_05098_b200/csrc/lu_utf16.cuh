@@ -330,36 +330,37 @@ __device__ __forceinline__ void u16u8_warp_r(const uint8_t *__restrict__ base, i
     constexpr int kRounds = kChunkBytes / 512;
     const uint4 *q = in.q;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(out_w);
-    uint32_t carry = in.halo_p;
-    const uint32_t halo_n = in.halo_n;
-    uint32_t rn[kRounds];
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r)
-        rn[r] = __shfl_sync(0xffffffffu, q[r].x, (lane + 1) & 31);
-
     uint32_t running = 0, err = 0, err_pos = 0, units = 0;
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
         const int64_t lane_off = chunk + r * 512 + 16 * (int64_t)lane;
-        const uint32_t rp = __shfl_sync(0xffffffffu, q[r].w, (lane + 31) & 31);
         uint32_t w[6];
-        w[0] = (lane == 0) ? carry : rp;
-        carry = rp;
+        w[0] = 0;
         w[1] = q[r].x;
         w[2] = q[r].y;
         w[3] = q[r].z;
         w[4] = q[r].w;
-        w[5] = (lane == 31) ? (r + 1 < kRounds ? rn[r + 1 < kRounds ? r + 1 : r] : halo_n) : rn[r];
-        // any surrogate among the lane's words (or a low surrogate right after
-        // them): high bytes gathered 4 words per register, D8..DF
+        w[5] = 0;
+        // any surrogate among the lane's words: high bytes gathered 4 words
+        // per register, D8..DF.  (A low surrogate right after the lane's
+        // words belongs to the next lane / round, which sees it itself.)
         uint32_t any;
         {
             const uint32_t c0 = hi_bytes(w[1], w[2]) ^ 0xD8D8D8D8u, c1 = hi_bytes(w[3], w[4]) ^ 0xD8D8D8D8u;
             const uint32_t u0 = (c0 & 0x78787878u) + 0x7F7F7F7Fu, u1 = (c1 & 0x78787878u) + 0x7F7F7F7Fu;
             any = (~(u0 | c0) | ~(u1 | c1)) & H8;
-            any |= is_ls(w[5] & 0xFFFFu) ? 1u : 0u;
         }
         const bool sur = __any_sync(0xffffffffu, any != 0);
+        if (sur) {
+            // only rounds with surrogates look at the words around a lane's
+            // quads (pairs that straddle lanes, rounds or the chunk)
+            const uint32_t rp = __shfl_sync(0xffffffffu, q[r].w, (lane + 31) & 31);
+            const uint32_t pr = r > 0 ? __shfl_sync(0xffffffffu, q[r > 0 ? r - 1 : 0].w, 31) : in.halo_p;
+            const uint32_t rx = __shfl_sync(0xffffffffu, q[r].x, (lane + 1) & 31);
+            const uint32_t nr = r + 1 < kRounds ? __shfl_sync(0xffffffffu, q[r + 1 < kRounds ? r + 1 : r].x, 0) : in.halo_n;
+            w[0] = lane == 0 ? pr : rp;
+            w[5] = lane == 31 ? nr : rx;
+        }
         // path C (warp-uniform, interior chunks): surrogates present, but every
         // word is ASCII or a surrogate and every pair is well formed (so no
         // error): a quad is at most 5 bytes -- the 4-byte forms of both
