@@ -266,12 +266,15 @@ def test_guard_bytes_around_misaligned_outputs(cuda_ok, utf16, be):
 # ------------------------------------------------------ full-size configs
 
 
-@pytest.mark.parametrize("profile", ["latin", "cyrillic", "cjk", "emoji"])
+@pytest.mark.parametrize("profile", ["latin", "cyrillic", "cjk", "emoji", "typo", "ascii", "mix"])
 def test_config2_config3_full_size(cuda_ok, profile):
-    """256 MiB buffers of each profile, both directions, against the oracle."""
+    """256 MiB buffers of each profile, both directions, against the oracle
+    (configs 2 / 3, plus the mixed-BMP, plain-ASCII and all-lengths profiles
+    that exercise the BMP class / path D, the ASCII chunk paths and the
+    general paths at full size)."""
     dev = torch.device("cuda", 0)
     n = 256 << 20
-    seed = {"latin": 1, "cyrillic": 2, "cjk": 3, "emoji": 4}[profile]
+    seed = {"latin": 1, "cyrillic": 2, "cjk": 3, "emoji": 4, "typo": 6, "ascii": 5, "mix": 0}[profile]
     src = corpus.generate(profile, n, seed, device=dev)
     res, out = transcode_device(UTF8_TO_UTF16, src)
     got = outcome_from_tensor(res.cpu())
