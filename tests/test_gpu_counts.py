@@ -102,7 +102,8 @@ def test_random_and_mutated(cuda_ok):
         check_u16(d.numpy().tobytes())
 
 
-@pytest.mark.parametrize("profile,seed", [("latin", 1), ("cyrillic", 2), ("cjk", 3), ("emoji", 4)])
+@pytest.mark.parametrize("profile,seed", [("latin", 1), ("cyrillic", 2), ("cjk", 3), ("emoji", 4), ("typo", 6),
+                                          ("ascii", 5), ("mix", 0)])
 def test_full_size_lengths_equal_transcode(cuda_ok, profile, seed):
     """256 MiB: the one-pass length equals the transcode's written count, and
     the char counts equal the oracle's."""
