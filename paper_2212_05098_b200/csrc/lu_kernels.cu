@@ -1241,6 +1241,11 @@ __global__ void __launch_bounds__(kThreads) k_batch(const uint8_t *__restrict__ 
 // not continuations, or words minus low surrogates.  No validation.  A plain
 // HBM-bound reduction: 16 bytes per thread per step, one atomic per warp.
 // ws layout: [u64 sum][u32 warps done][u32 pad].
+#ifndef LU_CHARS_UNROLL
+#define LU_CHARS_UNROLL 8
+#endif
+constexpr int kCharsUnroll = LU_CHARS_UNROLL; // 16-byte loads in flight per thread
+
 template <bool Utf16>
 __global__ void __launch_bounds__(kThreads) k_chars(const uint8_t *__restrict__ base, uint32_t lead, uint64_t n,
                                                     uint64_t *__restrict__ ws, uint64_t *__restrict__ out,
@@ -1249,7 +1254,40 @@ __global__ void __launch_bounds__(kThreads) k_chars(const uint8_t *__restrict__ 
     const int64_t lo_b = lead, hi_b = (int64_t)lead + (int64_t)(Utf16 ? 2 * n : n);
     const uint64_t stride = (uint64_t)gridDim.x * kThreads;
     uint64_t acc = 0;
-    for (uint64_t v = (uint64_t)blockIdx.x * kThreads + threadIdx.x; v < nvec; v += stride) {
+    uint64_t v = (uint64_t)blockIdx.x * kThreads + threadIdx.x;
+    // full vectors [vf0, vf1): kCharsUnroll independent 16-byte loads in flight per
+    // thread (64 B/thread reads ~7 TB/s where 16 B/thread stops at ~4.8,
+    // tools/probe/read_probe.cu); the ends go through the masked loop below
+    const uint64_t vf0 = (uint64_t)(lo_b + 15) / 16, vf1 = (uint64_t)hi_b / 16;
+    if (v >= vf0) {
+        for (; v + (kCharsUnroll - 1) * stride < vf1; v += kCharsUnroll * stride) {
+            uint4 q[kCharsUnroll];
+#pragma unroll
+            for (int j = 0; j < kCharsUnroll; ++j)
+                q[j] = __ldcs(reinterpret_cast<const uint4 *>(base + (int64_t)(v + j * stride) * 16));
+            // 128 x (continuation bytes | low surrogates) by dp4a, no POPC
+            uint32_t c = 0;
+#pragma unroll
+            for (int j = 0; j < kCharsUnroll; ++j) {
+                if (Utf16) {
+                    // high bytes of the vector's 8 words, 4 per register (as K4)
+                    uint32_t nhs, ls;
+                    u16_sur4(hi_bytes(q[j].x, q[j].y), nhs, ls);
+                    c = __dp4a(ls & H8, 0x01010101u, c);
+                    u16_sur4(hi_bytes(q[j].z, q[j].w), nhs, ls);
+                    c = __dp4a(ls & H8, 0x01010101u, c);
+                } else {
+                    const uint32_t w4[4] = {q[j].x, q[j].y, q[j].z, q[j].w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        c = __dp4a(w4[k] & ~(w4[k] << 1) & H8, 0x01010101u, c);
+                }
+            }
+            // u8: count the bytes that are NOT continuations; u16: the low surrogates
+            acc += Utf16 ? (c >> 7) : 16u * kCharsUnroll - (c >> 7);
+        }
+    }
+    for (; v < nvec; v += stride) {
         const int64_t a = (int64_t)v * 16;
         const bool full = a >= lo_b && a + 16 <= hi_b;
         const uint4 q =
