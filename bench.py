@@ -534,7 +534,10 @@ def main():
     # per-launch events (the roofline's launch durations) on every EV_EVERY-th
     # step of the timed region: a timing event pair costs ~4.5 us per launch
     # (measured, tools/rot_bench.py), which would otherwise inflate the step
-    ev_steps = list(range(0, args.steps, EV_EVERY))
+    # (starting at step EV_EVERY // 2, not 0: the first launch after the
+    # synchronize runs while the clocks ramp up from idle -- one ~2 ms sample in
+    # 50 moved the first profile's mean by 15-40 us)
+    ev_steps = list(range(min(EV_EVERY // 2, max(args.steps - 1, 0)), args.steps, EV_EVERY))
     evs = {k: [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in srcs]
            for k in ev_steps}
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -608,8 +611,8 @@ def main():
             "traffic_source": "profiles/ncu_summary.json (ncu --set full, dram__bytes_read+write per launch)",
             "peak_source": peak_src,
             "per_profile": prof_detail,
-            "launch_timing": f"CUDA events around each launch on every {EV_EVERY}th step of the timed region "
-            f"({len(ev_steps)} of {args.steps} steps)",
+            "launch_timing": f"CUDA events around each launch on every {EV_EVERY}th step of the timed region, "
+            f"from step {ev_steps[0] if ev_steps else 0} ({len(ev_steps)} of {args.steps} steps)",
         },
         "gpu_launches": args.steps * len(srcs),
         "clocks": clocks.summary(),
