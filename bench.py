@@ -750,6 +750,33 @@ def main():
                         "transcode_written": ot.written, "same_offset": ot.consumed == o.consumed}
             del ebuf
         extras["config4_validate"] = c4
+        # beyond the configs: plain ASCII (the paper's ASCII fast path) and mixed
+        # BMP text (accented Latin + typographic punctuation: no single class per
+        # chunk), 256 MiB each, all three hot kernels
+        log("extras: ascii / mixed-BMP profiles")
+        px = {}
+        for prof, seed in (("ascii", 5), ("typo", 6)):
+            u8 = corpus.generate(prof, BUF_BYTES, seed, device=dev)
+            u16 = corpus.generate(prof, BUF_BYTES // 2, seed, utf16=True, device=dev)
+            ent = {}
+            for name, fn, extra_of in (
+                    ("utf8_to_utf16", lambda r=None: transcode_device(UTF8_TO_UTF16, u8, outs[0], res=r), lambda o: 2 * o.written),
+                    ("utf16_to_utf8", lambda r=None: transcode_device(UTF16_TO_UTF8, u16, out8, res=r), lambda o: o.written),
+                    ("validate_utf8", lambda r=None: (validate_device(UTF8_TO_UTF16, u8, res=r), None), lambda o: 0)):
+                res = fn()[0]
+                o = outcome_from_tensor(res.cpu())
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(k_ex):
+                    fn(res)
+                b.record(stream)
+                torch.cuda.synchronize()
+                t = a.elapsed_time(b) / 1e3 / k_ex
+                ent[name] = {"input_gib_s": round(BUF_BYTES / GIB / t, 2),
+                             "frac_of_measured": round((BUF_BYTES + extra_of(o)) / t / 1e9 / peak, 4), "ok": o.ok}
+            px[prof] = ent
+            del u8, u16
+        extras["ascii_and_mixed_bmp_profiles"] = px
         # config 1: UTF-8 -> UTF-16LE -> UTF-8 round trip of the 4 MiB mixed
         # buffer (seed 0): two launches of a latency-bound size
         log("extras: config 1")
